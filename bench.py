@@ -1,0 +1,379 @@
+"""Benchmark: symmetric-contraction fwd+bwd nodes/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config mp_medium]
+
+A step is one pass of the whole hot path over one bin of molecular graphs per GPU:
+element bucketing, W-fold, forward B, backward dW (S partials + fixed-order reduction) and
+dA, and — for N > 1 — the NCCL all-reduce of dW. Workload (SURVEY.md §8(d) config 5 at the
+MP-medium shape): the 2,650,823-graph Table-2 manifest packed by Alg. 1 (C++ partitioner,
+capacity 50,000 nodes, M = multiple of N bins), bin s*N + r on rank r at step s; 128
+channels, 0e+1o output, lmax 3, correlation 3, 89 elements (1-4 Zipf elements per graph).
+Inputs for the timed steps are resident in HBM before timing; A alone is 410 MB per bin,
+larger than L2, and a pool of distinct bins is cycled, so no L2 flush is needed.
+
+One JSON line on rank 0. `roofline` reports the dominant kernel (FP32 ALU bound), its
+per-launch CUDA-event time measured by libsymcon's launch timer inside the timed region.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CAPACITY = 50_000
+POOL = 4
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="mp_medium", choices=["off_small", "mp_medium", "large"])
+    ap.add_argument("--cpu-sample", type=int, default=4096, help="nodes in the oracle's bounded sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- workload
+def shape_of(name):
+    from synth.inputs import CONFIGS
+    return CONFIGS[name]
+
+
+def plan_bins(world, seed=0):
+    """Alg. 1 over the Table-2 manifest (same plan on every rank: deterministic)."""
+    from synth.inputs import table2_sizes
+    from paper_2504_10700_b200 import _lib
+    sizes = table2_sizes(seed=seed)
+    t0 = time.time()
+    offs, ids = _lib.symcon_pack_balanced(sizes, CAPACITY, world)
+    return sizes, offs, ids, time.time() - t0
+
+
+def bin_elements(sizes, offs, ids, b, n_elements):
+    from synth.inputs import graph_elements
+    g = ids[offs[b]:offs[b + 1]]
+    return graph_elements(sizes[g], n_elements=n_elements, seed=0, salt=int(b))
+
+
+def alg_ops(sc):
+    """Algorithmic FP32 lane-ops per (node, channel) per kernel, from the plan's tables
+    (DESIGN.md §8): products = distinct (a,b) prefixes + degree-3 monomials; fold = rows;
+    partials = sum over monomials of distinct factors."""
+    from paper_2504_10700_b200 import _lib
+    L, M, mono, col, val = _lib.symcon_plan_sym_table(sc.plan)
+    rows = {(int(L[i]), int(M[i]), tuple(int(x) for x in mono[i])) for i in range(len(L))}
+    monos = {r[2] for r in rows}
+    prefixes = {m[:2] for m in monos if m[1] >= 0}
+    deg3 = [m for m in monos if m[2] >= 0]
+    products = len(prefixes) + len(deg3)
+    partials = sum(len({x for x in m if x >= 0}) for m in monos)
+    n_fold = len(rows)
+    return {"fwd": products + n_fold, "dA": products + n_fold + partials, "dW": products + n_fold,
+            "path": 2 * products + 3 * n_fold + partials, "n_fold": n_fold, "products": products,
+            "partials": partials, "n_sym": int(len(L))}
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = "index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p:
+            time.sleep(0.25)
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        load = [s for s in sm if mx and s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- cpu oracle
+def cpu_baseline(cfg, sc, A, W, ne, dB, n_sample, seed=0):
+    """The oracle's plain C fp64 loop (never tuned) on a bounded sample of the workload."""
+    from oracle.contraction import Problem
+    from oracle.ceval import OracleC
+    oc = OracleC(Problem(cfg.lmax_in, cfg.correlation, cfg.out_L))
+    rng = np.random.default_rng(seed)
+    idx = np.sort(rng.choice(A.shape[0], min(n_sample, A.shape[0]), replace=False))
+    import torch
+    ti = torch.from_numpy(idx).to(A.device)
+    hA, hne, hdB = A[ti].cpu().numpy(), ne[ti].cpu().numpy(), dB[ti].cpu().numpy()
+    hW = W.cpu().numpy()
+    t0 = time.time()
+    oc.forward(hA, hW, hne)
+    oc.backward(hA, hW, hne, hdB)
+    dt = time.time() - t0
+    return {"value": len(idx) / dt, "unit": "nodes/s", "cores": oc.threads(), "kind": "oracle",
+            "sample": f"{len(idx)} random nodes of one {A.shape[0]}-node bin, fwd+bwd (B, dA, dW), fp64 C/OpenMP loop "
+                      f"over {oc.n_terms} raw U terms per (node, channel), {dt:.1f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle on the host cores, each step a bounded sample of the workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+    from synth.inputs import gen_A, gen_W, gen_dB
+    from oracle.contraction import Problem
+    from oracle.ceval import OracleC
+    cfg = shape_of(args.config)
+    prob = Problem(cfg.lmax_in, cfg.correlation, cfg.out_L)
+    oc = OracleC(prob)
+    sizes, offs, ids, _ = plan_bins(max(args.gpus, 1))
+    ne_full = bin_elements(sizes, offs, ids, 0, cfg.n_elements)
+    n_bin = len(ne_full)
+    per_step = max(64, args.cpu_sample // 8)
+    A = gen_A(per_step, cfg.channels, 16, "cpu").numpy()
+    W = gen_W(cfg.n_elements, prob.block_sizes(), cfg.channels, "cpu").numpy()
+    dB = gen_dB(per_step, prob.out_dim(cfg.channels), "cpu").numpy()
+    ne = ne_full[:per_step]
+    for _ in range(args.warmup):
+        oc.forward(A[:16], W, ne[:16])
+    t0 = time.time()
+    for _ in range(args.steps):
+        oc.forward(A, W, ne)
+        oc.backward(A, W, ne, dB)
+    dt = time.time() - t0
+    v = per_step * args.steps / dt
+    out = {"impl": "reference", "metric": "symcon_fwd_bwd_nodes_per_s", "value": v, "unit": "nodes/s",
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"{args.config}_dp_step", "nodes_per_bin": n_bin, "channels": cfg.channels,
+                      "out": "+".join(f"{L}{'e' if L % 2 == 0 else 'o'}" for L in cfg.out_L), "lmax_in": cfg.lmax_in,
+                      "correlation": cfg.correlation, "elements": cfg.n_elements,
+                      "sample": f"{per_step} nodes of bin 0 per step"},
+           "cpu_baseline": {"value": v, "unit": "nodes/s", "cores": oc.threads(), "kind": "oracle",
+                            "sample": f"{per_step} nodes per step x {args.steps} steps"},
+           "e2e": {"value": v, "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ----------------------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != max(args.gpus, 1) and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2504_10700_b200.ops import SymmetricContraction
+    from paper_2504_10700_b200 import _lib
+    from synth.inputs import gen_A, gen_W, gen_dB
+    cfg = shape_of(args.config)
+    sc = SymmetricContraction(cfg.lmax_in, cfg.correlation, cfg.out_L, cfg.n_elements, cfg.channels, device=local)
+    _lib.symcon_profile_enable(sc.plan, 1)
+
+    sizes, offs, ids, t_pack = plan_bins(world)
+    n_bins = len(offs) - 1
+    steps_avail = n_bins // world
+    # pool of distinct bins for this rank (cycled)
+    pool = []
+    for q in range(POOL):
+        b = (q % steps_avail) * world + rank
+        ne = torch.from_numpy(bin_elements(sizes, offs, ids, b, cfg.n_elements)).to(dev)
+        N = ne.numel()
+        A = gen_A(N, cfg.channels, sc.n_lm, dev, seed=100 * q + rank)
+        dB = gen_dB(N, sc.out_dim, dev, seed=100 * q + rank)
+        B = torch.empty((N, sc.out_dim), device=dev)
+        dA = torch.empty_like(A)
+        pool.append((b, N, A, ne, dB, B, dA))
+    W = gen_W(cfg.n_elements, sc.block_sizes(), cfg.channels, dev)
+    if world > 1:
+        dist.broadcast(W, 0)
+    dW = torch.empty_like(W)
+    for q in range(POOL):
+        sc.workspace(pool[q][1])
+
+    launches = [0]
+
+    def step(q):
+        b, N, A, ne, dB, B, dA = pool[q % POOL]
+        sc.forward_raw(A, W, ne, B=B)
+        launches[0] += sc.last_launch_count()
+        sc.backward_raw(A, W, ne, dB, dA=dA, dW=dW)
+        launches[0] += sc.last_launch_count()
+        if world > 1:
+            dist.all_reduce(dW)
+        return N
+
+    for q in range(args.warmup):
+        step(q)
+    torch.cuda.synchronize()
+    s, bad = sc.check_device_error()
+    assert s == 0, (s, bad)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    _lib.symcon_profile_reset(sc.plan)
+    launches[0] = 0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nodes = 0
+    with ClockSampler(local) as clk:
+        e0.record()
+        for q in range(args.steps):
+            nodes += step(q)
+        e1.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    prof = _lib.symcon_profile_read(sc.plan)
+    t = torch.tensor([ms, nodes], dtype=torch.float64, device=dev)
+    if world > 1:
+        tt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(tt, t)
+        ms_max = max(float(x[0]) for x in tt)
+        nodes_all = sum(float(x[1]) for x in tt)
+    else:
+        ms_max, nodes_all = ms, float(nodes)
+    value = nodes_all / (ms_max / 1e3)
+
+    # ---- e2e through the public API with host buffers (pinned), copies inside the timed region
+    b, N, A, ne, dB, B, dA = pool[0]
+    hA, hne, hdB = A.cpu().pin_memory(), ne.cpu().pin_memory(), dB.cpu().pin_memory()
+    hdW = torch.empty(W.shape, dtype=W.dtype).pin_memory()
+    dA2, dB2, ne2 = torch.empty_like(A), torch.empty_like(dB), torch.empty_like(ne)
+    A2 = torch.empty_like(A)
+
+    def e2e_step():
+        A2.copy_(hA, non_blocking=True)
+        ne2.copy_(hne, non_blocking=True)
+        dB2.copy_(hdB, non_blocking=True)
+        Bx = sc.forward_raw(A2, W, ne2, B=B)
+        sc.backward_raw(A2, W, ne2, dB2, dA=dA2, dW=dW)
+        if world > 1:
+            dist.all_reduce(dW)
+        hdW.copy_(dW, non_blocking=True)
+        return Bx
+
+    e2e_steps = max(3, min(args.steps, 10))
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    for _ in range(e2e_steps):
+        e2e_step()
+    f1.record()
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1) / e2e_steps
+    t2 = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+    e2e_value = N * world / (float(t2[0]) / 1e3)
+    h2d = hA.numel() * 4 + hne.numel() * 4 + hdB.numel() * 4
+    d2h = hdW.numel() * 4
+
+    if rank == 0:
+        ops = alg_ops(sc)
+        K = cfg.channels
+        clocks = clk.summary()
+        # dominant kernel by measured time
+        kern = max(prof, key=lambda k: prof[k][1]) if prof else None
+        roof = None
+        if kern:
+            cnt, tot_ms = prof[kern]
+            avg_ms = tot_ms / max(cnt, 1)
+            per_nc = {"symcon_fwd": ops["fwd"], "symcon_bwd_dA": ops["dA"], "symcon_bwd_dW": ops["dW"]}.get(kern)
+            mean_nodes = nodes / args.steps
+            if per_nc:
+                achieved = per_nc * mean_nodes * K / (avg_ms / 1e3) / 1e12  # T lane-ops/s
+                sm_mhz = 1965.0
+                peak = 148 * 128 * sm_mhz * 1e6 / 1e12
+                roof = {"bound": "alu", "kernel": kern, "achieved": achieved, "peak": peak, "unit": "Tops/s (fp32 FMA lane-ops)",
+                        "frac": achieved / peak, "traffic": None, "avg_launch_ms": avg_ms,
+                        "ops_per_node_channel": per_nc,
+                        "peak_derivation": "148 SMs x 128 FP32 lanes x 1965 MHz (clocks.max.sm); FFMA probe measured 36.0 T/s"}
+        path_ops = ops["path"] * (nodes / args.steps) * K
+        kernels = {k: {"launches": v[0], "avg_ms": v[1] / max(v[0], 1)} for k, v in prof.items()}
+        out = {
+            "metric": "symcon_fwd_bwd_nodes_per_s", "value": value, "unit": "nodes/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{args.config}_dp_step", "model": "MACE symmetric contraction",
+                       "channels": K, "out": "+".join(f"{K}x{L}{'e' if L % 2 == 0 else 'o'}" for L in cfg.out_L),
+                       "lmax_in": cfg.lmax_in, "correlation": cfg.correlation, "elements": cfg.n_elements,
+                       "capacity_nodes": CAPACITY, "bins": n_bins, "global_batch": int(nodes_all / args.steps),
+                       "seq_len": None, "parallelism": f"dp{world}", "l2": "inputs > L2 (A 410 MB/bin), 4-bin pool",
+                       "alg1_pack_s": round(t_pack, 3)},
+            "per_gpu_nodes_per_s": value / world,
+            "path_tops": path_ops / (ms_max / args.steps / 1e3) / 1e12,
+            "path_frac_of_alu_peak": path_ops / (ms_max / args.steps / 1e3) / 1e12 / (148 * 128 * 1.965e-3),
+            "roofline": roof, "kernels": kernels, "alg_ops_per_node_channel": ops,
+            "clocks": clocks, "gpu_launches": launches[0],
+            "e2e": {"value": e2e_value, "unit": "nodes/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "note": "H2D A+node_elem+dB from pinned host, D2H dW, per step through SymmetricContraction"},
+        }
+        if not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(cfg, sc, A, W, ne, dB, args.cpu_sample)
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,154 @@
+/* symcon.h — C ABI of libsymcon.so: MACE's symmetric tensor contraction on B200 (sm_100a).
+ *
+ * Operation (arXiv 2504.10700, Alg. 3; Eq. (2)):
+ *   for node i, channel k, output irrep L in out_L, component M:
+ *     B[i,k,(L,M)] = sum_{nu=1..correlation} sum_eta W[z_i,(L,nu,eta),k]
+ *                    * sum_{lm_1..lm_nu} U^{LM}_{nu,eta,lm_1..lm_nu} * prod_j A[i,k,lm_j]
+ *   U is the generalized real Clebsch-Gordan coefficient C^{LM}_{lm},
+ *   read as a left-nested chain of pairwise real couplings (DESIGN.md §3 reading s4), with
+ *   the CG selection rules of PAPER.md:696-697. W is per element ("depends on the atomic
+ *   species z_i"). Backward: dA (forces are derivatives of the energy,
+ *   PAPER.md:331) and dW.
+ *
+ * Layouts (all row-major, fp32 unless noted):
+ *   A, dA     [N][K][(lmax_in+1)^2]            lm = l*l + l + m fastest
+ *   B, dB     [N][sum_L K*(2L+1)]              per-L block [K][2L+1], blocks in out_L order
+ *   W, dW     [E][P][K]                        P = symcon_info.n_paths; columns ordered by
+ *                                              out_L, then nu, then eta (symcon_plan_path)
+ *   node_elem int32 [N], values in [0, E)
+ *
+ * Ownership: the caller owns every device buffer (A, W, node_elem, B, dA, dB, dW and the
+ * workspace); the library owns only the plan (host tables, device tables, loaded kernels),
+ * freed by symcon_destroy. All device pointers live on the plan's device. Calls are
+ * asynchronous on the given stream; no host synchronisation except where stated.
+ *
+ * Errors: invalid arguments are reported synchronously (before any launch) as
+ * SYMCON_EINVAL / SYMCON_EUNSUPPORTED; CUDA launch failures as SYMCON_ECUDA. An
+ * out-of-range node_elem value is detected on the device: that node's outputs (B row, dA
+ * row) are set to NaN, it contributes nothing to dW, and the first offending node index is
+ * recorded in the workspace; symcon_check_device_error (synchronising) returns
+ * SYMCON_EELEMENT for it ("species index without weights -> validation error").
+ *
+ * Determinism: no floating-point atomics; dW is reduced in a fixed order, so all outputs
+ * are bitwise reproducible for a given (plan, N, node_elem, inputs, device).
+ * Thread-safety: a plan is immutable after symcon_build_tables; concurrent calls on
+ * different streams are allowed when each call has its own workspace.
+ */
+#ifndef SYMCON_H
+#define SYMCON_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SYMCON_OK = 0,
+  SYMCON_EINVAL = 1,       /* bad argument (null pointer, size, alignment, range) */
+  SYMCON_EUNSUPPORTED = 2, /* valid but not supported (e.g. correlation > 3) */
+  SYMCON_ECUDA = 3,        /* CUDA / NVRTC failure */
+  SYMCON_ENOMEM = 4,       /* host allocation or workspace too small */
+  SYMCON_EELEMENT = 5      /* node_elem value outside [0, E) found on the device */
+} symcon_status;
+
+typedef struct symcon_plan symcon_plan; /* opaque */
+
+typedef struct {
+  int32_t lmax_in, correlation, n_out, num_elements, channels;
+  int32_t out_L[4];
+  int32_t eta[4][4];     /* eta[out index][nu-1]: number of paths */
+  int64_t n_paths;       /* P: W middle dimension */
+  int64_t weight_numel;  /* E * P * K */
+  int64_t in_dim;        /* K * (lmax_in+1)^2  per node */
+  int64_t out_dim;       /* K * sum_L (2L+1)   per node */
+  int64_t n_raw_terms;   /* raw ordered-tuple U nonzeros, all paths */
+  int64_t n_sym_terms;   /* (L,M,monomial,path) nonzeros after symmetrisation */
+  int64_t n_fold;        /* (L,M,monomial) rows: folded coefficients per (element, channel) */
+  int64_t n_monomials;   /* distinct monomials of A used */
+  int32_t device;        /* -1: host-only plan (tables, no kernels) */
+  int32_t reserved;
+} symcon_info;
+
+/* Build the U tables for (lmax_in, correlation, out_L[0..n_out)) and, if device >= 0,
+ * generate, compile (NVRTC, sm_100a; cached on disk) and load the kernels for that device.
+ *   lmax_in in [0,3]; correlation in [1,3]; out_L strictly increasing, each in [0,3],
+ *   n_out in [1,4]; num_elements >= 1; channels >= 1.
+ *   device = -1 builds host tables only (for inspection; compute calls return EINVAL).
+ * On success *plan is owned by the caller and must be freed with symcon_destroy. */
+symcon_status symcon_build_tables(int lmax_in, int correlation, const int* out_L, int n_out,
+                                  int num_elements, int channels, int device, symcon_plan** plan);
+
+symcon_status symcon_plan_info(const symcon_plan* plan, symcon_info* info);
+
+/* Describe W column `col` in [0, P): its output L, order nu, index eta, the coupled
+ * irreps ls[0..nu) and the intermediates mids[0..nu-1) (mids[nu-2] == L for nu >= 2). */
+symcon_status symcon_plan_path(const symcon_plan* plan, int64_t col, int32_t* L, int32_t* nu,
+                               int32_t* eta, int32_t* ls, int32_t* mids);
+
+/* Copy the symmetrised table (host): rows (L, M, monomial a<=b<=c padded with -1, path
+ * column, value). Pass NULL arrays to query the count into *n. Used by table-parity tests. */
+symcon_status symcon_plan_sym_table(const symcon_plan* plan, int64_t* n, int32_t* L, int32_t* M,
+                                    int32_t* mono3, int32_t* col, double* value);
+
+/* Copy the pairwise real coupling C^L_{l1 l2}[M][m1][m2] (host) into out
+ * [(2L+1)(2l1+1)(2l2+1)] (zeros if the triangle rule fails). l1,l2 <= 3, L <= 6. */
+symcon_status symcon_real_cg(int l1, int l2, int L, double* out);
+
+/* Workspace bytes needed by forward/backward for num_nodes nodes (16-byte aligned). */
+size_t symcon_workspace_bytes(const symcon_plan* plan, int64_t num_nodes);
+
+/* Forward: B (overwritten) from A, W, node_elem. N = 0 is a no-op. A and B 16-byte
+ * aligned. ws must hold symcon_workspace_bytes(plan, num_nodes) bytes. */
+symcon_status symcon_forward(const symcon_plan* plan, int64_t num_nodes, const float* A,
+                             const float* W, const int32_t* node_elem, float* B, void* ws,
+                             size_t ws_bytes, void* stream /* cudaStream_t */);
+
+/* Backward: dA (overwritten, may be NULL to skip) and dW (overwritten, may be NULL to skip)
+ * from A, W, node_elem and the cotangent dB. Elements without nodes get dW = 0. */
+symcon_status symcon_backward(const symcon_plan* plan, int64_t num_nodes, const float* A,
+                              const float* W, const int32_t* node_elem, const float* dB, float* dA,
+                              float* dW, void* ws, size_t ws_bytes, void* stream /* cudaStream_t */);
+
+/* Synchronises `stream`; returns SYMCON_EELEMENT and *first_bad_node if the last forward /
+ * backward that used `ws` saw an out-of-range node_elem, SYMCON_ECUDA on a CUDA error. */
+symcon_status symcon_check_device_error(const symcon_plan* plan, void* ws, void* stream,
+                                        int64_t* first_bad_node);
+
+/* Kernel launches the last forward/backward on this plan issued (for bench accounting). */
+int32_t symcon_last_launch_count(const symcon_plan* plan);
+
+/* Optional launch timer for benchmarking: when enabled, every launch group (bucket, fold,
+ * fwd, bwd_dA, bwd_dW, unfold, fill_nan) is bracketed by CUDA events on its stream.
+ * symcon_profile_read synchronises those events and returns up to 8 entries of
+ * (kernel name, launches, total milliseconds); names point to static strings. */
+symcon_status symcon_profile_enable(const symcon_plan* plan, int on);
+symcon_status symcon_profile_reset(const symcon_plan* plan);
+int32_t symcon_profile_read(const symcon_plan* plan, const char** names, int64_t* counts, double* total_ms);
+
+/* Build-host helpers (no device needed): NVRTC-compile a configuration's kernels into the
+ * cubin cache and report its path; copy a plan's generated CUDA source (NULL buf: size). */
+symcon_status symcon_precompile(int lmax_in, int correlation, const int* out_L, int n_out, char* path,
+                                size_t path_len);
+size_t symcon_plan_source(const symcon_plan* plan, char* buf, size_t len);
+
+void symcon_destroy(symcon_plan* plan);
+const char* symcon_status_string(symcon_status s);
+/* Human-readable detail of the last error in this thread (never NULL). */
+const char* symcon_last_error(void);
+
+/* ---- host partitioner (Alg. 1 Create-Balanced-Batches) -------------
+ * sizes[n] >= 0 (graph vertex counts), capacity C, workers G >= 1. Produces bins in
+ * creation order: bin b holds graph_ids[bin_offsets[b] .. bin_offsets[b+1]).
+ * Bin b runs on rank b % G at step b / G (reading s18). Deterministic.
+ * Any size > C -> SYMCON_EINVAL. If max_bins is too small -> SYMCON_ENOMEM with *n_bins
+ * set to the required count. bin_offsets needs max_bins+1 entries, graph_ids n entries. */
+symcon_status symcon_pack_balanced(const int64_t* sizes, int64_t n, int64_t capacity,
+                                   int32_t workers, int64_t* bin_offsets, int64_t* graph_ids,
+                                   int64_t max_bins, int64_t* n_bins);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SYMCON_H */

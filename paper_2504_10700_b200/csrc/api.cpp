@@ -1,0 +1,632 @@
+// C ABI of libsymcon (include/symcon.h): plan construction, NVRTC kernel compilation with an
+// on-disk cubin cache, workspace carving and the forward / backward launch sequences.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nvrtc.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "kernels.h"
+
+namespace symcon {
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace symcon
+
+using namespace symcon;
+
+struct symcon_plan {
+  Tables t;
+  KernelConfig kc;
+  int device = -1;
+  int npad = 0;
+  std::string source;
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t k_fold = nullptr, k_fwd = nullptr, k_dA = nullptr, k_dW = nullptr, k_unfold = nullptr;
+  mutable std::atomic<int> last_launches{0};
+  // optional launch timer (symcon_profile_*): CUDA events around each launch group
+  struct Rec { int kind; cudaEvent_t a, b; };
+  mutable std::mutex prof_mu;
+  mutable bool prof_on = false;
+  mutable std::vector<Rec> recs;
+  mutable std::vector<cudaEvent_t> event_pool;
+  mutable double prof_ms[8] = {0};
+  mutable int64_t prof_n[8] = {0};
+};
+
+static const char* kKindNames[] = {"symcon_bucket", "symcon_fold", "symcon_fwd", "symcon_bwd_dA", "symcon_bwd_dW",
+                                   "symcon_unfold", "symcon_fill_nan", "other"};
+enum { K_BUCKET = 0, K_FOLD, K_FWD, K_DA, K_DW, K_UNFOLD, K_NAN };
+
+namespace {
+cudaEvent_t take_event(const symcon_plan* p) {
+  if (!p->event_pool.empty()) { cudaEvent_t e = p->event_pool.back(); p->event_pool.pop_back(); return e; }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+void drain(const symcon_plan* p) {  // caller holds prof_mu
+  for (auto& r : p->recs) {
+    float ms = 0;
+    if (cudaEventSynchronize(r.b) == cudaSuccess && cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+      p->prof_ms[r.kind] += ms;
+      p->prof_n[r.kind]++;
+    }
+    p->event_pool.push_back(r.a);
+    p->event_pool.push_back(r.b);
+  }
+  p->recs.clear();
+}
+struct Timed {  // RAII: records start/stop events around a launch group when profiling is on
+  const symcon_plan* p; int kind; cudaStream_t st; cudaEvent_t a = nullptr, b = nullptr;
+  Timed(const symcon_plan* p_, int k, cudaStream_t s) : p(p_), kind(k), st(s) {
+    if (!p->prof_on) return;
+    std::lock_guard<std::mutex> g(p->prof_mu);
+    if (p->recs.size() > 4096) drain(p);
+    a = take_event(p); b = take_event(p);
+    cudaEventRecord(a, st);
+  }
+  ~Timed() {
+    if (!a) return;
+    cudaEventRecord(b, st);
+    std::lock_guard<std::mutex> g(p->prof_mu);
+    p->recs.push_back({kind, a, b});
+  }
+};
+}  // namespace
+
+namespace {
+
+struct Params {  // must match SymconParams in codegen.cpp
+  const float* A; const float* W; const int* node_elem; const float* dB;
+  float* B; float* dA; float* dW;
+  const int* perm; const int4* tiles; const int* n_tiles; const int4* items; const int* n_items;
+  const int* item_off; const int* seg_off;
+  float* coef; float* spart;
+  int N, K, E, pad;
+};
+
+struct WsLayout {
+  size_t hist, off, seg_off, perm, tiles, n_tiles, items, n_items, item_off, err, coef, spart, total;
+  int64_t max_tiles, max_items;
+};
+
+size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+WsLayout layout(const symcon_plan* p, int64_t N) {
+  WsLayout w{};
+  const int E = p->t.E, K = p->t.K;
+  const size_t nch = bucket_chunks(N);
+  w.max_tiles = N / p->kc.tile_nodes + E + 1;
+  w.max_items = w.max_tiles / p->kc.dw_tiles_per_item + E + 1;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes); return r; };
+  w.err = take(sizeof(unsigned long long));  // first: its offset must not depend on N
+  w.hist = take(sizeof(int) * nch * (E + 1));
+  w.off = take(sizeof(int) * nch * (E + 1));
+  w.seg_off = take(sizeof(int) * (E + 2));
+  w.perm = take(sizeof(int) * std::max<int64_t>(N, 1));
+  w.tiles = take(sizeof(int4) * w.max_tiles);
+  w.n_tiles = take(sizeof(int));
+  w.items = take(sizeof(int4) * w.max_items);
+  w.n_items = take(sizeof(int));
+  w.item_off = take(sizeof(int) * (E + 2));
+  w.coef = take(sizeof(float) * (size_t)E * K * p->npad);
+  w.spart = take(sizeof(float) * (size_t)w.max_items * K * p->npad);
+  w.total = o;
+  return w;
+}
+
+uint64_t fnv1a(const std::string& s) {
+  uint64_t h = 1469598103934665603ull;
+  for (unsigned char c : s) { h ^= c; h *= 1099511628211ull; }
+  return h;
+}
+
+std::string lib_dir() {
+  Dl_info info;
+  if (dladdr((void*)&symcon_status_string, &info) && info.dli_fname) {
+    std::string f = info.dli_fname;
+    auto pos = f.rfind('/');
+    if (pos != std::string::npos) return f.substr(0, pos);
+  }
+  return ".";
+}
+
+std::string cache_dir() {
+  const char* e = getenv("SYMCON_KCACHE");
+  std::string d = e && *e ? e : lib_dir() + "/_kcache";
+  mkdir(d.c_str(), 0775);
+  return d;
+}
+
+const std::vector<std::string>& nvrtc_opts() {
+  static std::vector<std::string> o = {"--gpu-architecture=sm_100a", "-lineinfo", "--std=c++17",
+                                       "--ptxas-options=-v", "-DSYMCON_GENERATED=1"};
+  return o;
+}
+
+std::mutex g_compile_mu;
+
+// returns cubin bytes; compiles with NVRTC and caches on disk
+bool get_cubin(const std::string& src, std::vector<char>& cubin, std::string* path_out) {
+  std::string key = src;
+  for (auto& s : nvrtc_opts()) key += "\n" + s;
+  int maj = 0, min = 0;
+  nvrtcVersion(&maj, &min);
+  key += "\nnvrtc" + std::to_string(maj) + "." + std::to_string(min);
+  char name[64];
+  snprintf(name, sizeof name, "symcon_%016llx", (unsigned long long)fnv1a(key));
+  std::string dir = cache_dir();
+  std::string path = dir + "/" + name + ".cubin";
+  if (path_out) *path_out = path;
+  std::lock_guard<std::mutex> g(g_compile_mu);
+  {
+    std::ifstream f(path, std::ios::binary);
+    if (f) {
+      cubin.assign(std::istreambuf_iterator<char>(f), std::istreambuf_iterator<char>());
+      if (!cubin.empty()) return true;
+    }
+  }
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, src.c_str(), "symcon_generated.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+    set_error("nvrtcCreateProgram failed");
+    return false;
+  }
+  std::vector<const char*> opts;
+  for (auto& s : nvrtc_opts()) opts.push_back(s.c_str());
+  nvrtcResult r = nvrtcCompileProgram(prog, (int)opts.size(), opts.data());
+  size_t logsz = 0;
+  nvrtcGetProgramLogSize(prog, &logsz);
+  std::string log(logsz, '\0');
+  if (logsz) nvrtcGetProgramLog(prog, &log[0]);
+  if (r != NVRTC_SUCCESS) {
+    set_error("NVRTC compile failed: " + log.substr(0, 4000));
+    std::ofstream(dir + "/" + name + ".failed.cu") << src;
+    nvrtcDestroyProgram(&prog);
+    return false;
+  }
+  size_t n = 0;
+  nvrtcGetCUBINSize(prog, &n);
+  cubin.resize(n);
+  nvrtcGetCUBIN(prog, cubin.data());
+  nvrtcDestroyProgram(&prog);
+  std::string tmp = path + ".tmp" + std::to_string(getpid());
+  {
+    std::ofstream f(tmp, std::ios::binary);
+    f.write(cubin.data(), (std::streamsize)cubin.size());
+  }
+  rename(tmp.c_str(), path.c_str());
+  std::ofstream(dir + "/" + name + ".log") << log;
+  std::ofstream(dir + "/" + name + ".cu") << src;
+  return true;
+}
+
+symcon_status cuda_err(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return SYMCON_OK;
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return SYMCON_ECUDA;
+}
+
+bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+symcon_status validate_build(int lmax_in, int corr, const int* out_L, int n_out, int E, int K) {
+  if (lmax_in < 0 || lmax_in > 3) { set_error("lmax_in must be in [0,3]"); return SYMCON_EINVAL; }
+  if (corr < 1) { set_error("correlation must be >= 1"); return SYMCON_EINVAL; }
+  if (corr > 3) { set_error("correlation > 3 is not supported (needs the intermediate-irrep filter)"); return SYMCON_EUNSUPPORTED; }
+  if (!out_L || n_out < 1 || n_out > 4) { set_error("n_out must be in [1,4]"); return SYMCON_EINVAL; }
+  for (int i = 0; i < n_out; i++) {
+    if (out_L[i] < 0 || out_L[i] > 3) { set_error("out_L values must be in [0,3]"); return SYMCON_EINVAL; }
+    if (i && out_L[i] <= out_L[i - 1]) { set_error("out_L must be strictly increasing"); return SYMCON_EINVAL; }
+  }
+  if (E < 1 || E > 8192) { set_error("num_elements must be in [1, 8192]"); return SYMCON_EINVAL; }
+  if (K < 1 || K > (1 << 20)) { set_error("channels must be >= 1"); return SYMCON_EINVAL; }
+  return SYMCON_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* symcon_status_string(symcon_status s) {
+  switch (s) {
+    case SYMCON_OK: return "ok";
+    case SYMCON_EINVAL: return "invalid argument";
+    case SYMCON_EUNSUPPORTED: return "unsupported";
+    case SYMCON_ECUDA: return "CUDA error";
+    case SYMCON_ENOMEM: return "out of memory / workspace too small";
+    case SYMCON_EELEMENT: return "node_elem out of range (species index without weights)";
+  }
+  return "unknown";
+}
+
+const char* symcon_last_error(void) { return g_last_error.c_str(); }
+
+symcon_status symcon_real_cg(int l1, int l2, int L, double* out) {
+  if (!out || l1 < 0 || l2 < 0 || L < 0 || l1 > 3 || l2 > 3 || L > 6) { set_error("bad l"); return SYMCON_EINVAL; }
+  auto c = real_coupling(l1, l2, L);
+  std::memcpy(out, c.data(), c.size() * sizeof(double));
+  return SYMCON_OK;
+}
+
+static symcon_status build_common(int lmax_in, int corr, const int* out_L, int n_out, int E, int K, symcon_plan** out) {
+  symcon_status s = validate_build(lmax_in, corr, out_L, n_out, E, K);
+  if (s) return s;
+  auto* p = new (std::nothrow) symcon_plan();
+  if (!p) return SYMCON_ENOMEM;
+  std::vector<int> ol(out_L, out_L + n_out);
+  if (!build_tables(lmax_in, corr, ol, E, K, p->t)) { delete p; return SYMCON_EINVAL; }
+  p->npad = (int)((p->t.rows.size() + 31) / 32 * 32);
+  p->source = generate_source(p->t, p->kc);
+  *out = p;
+  return SYMCON_OK;
+}
+
+symcon_status symcon_build_tables(int lmax_in, int correlation, const int* out_L, int n_out, int num_elements,
+                                  int channels, int device, symcon_plan** plan) {
+  if (!plan) { set_error("plan is NULL"); return SYMCON_EINVAL; }
+  *plan = nullptr;
+  symcon_plan* p = nullptr;
+  symcon_status s = build_common(lmax_in, correlation, out_L, n_out, num_elements, channels, &p);
+  if (s) return s;
+  p->device = device;
+  if (device >= 0) {
+    int ndev = 0;
+    if ((s = cuda_err(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount"))) { delete p; return s; }
+    if (device >= ndev) { set_error("device out of range"); delete p; return SYMCON_EINVAL; }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    int maj = 0, mnr = 0;
+    cudaDeviceGetAttribute(&maj, cudaDevAttrComputeCapabilityMajor, device);
+    cudaDeviceGetAttribute(&mnr, cudaDevAttrComputeCapabilityMinor, device);
+    if (maj != 10 || mnr != 0) {
+      set_error("libsymcon kernels are built for sm_100a (B200); device is sm_" + std::to_string(maj) + std::to_string(mnr));
+      cudaSetDevice(prev);
+      delete p;
+      return SYMCON_EUNSUPPORTED;
+    }
+    std::vector<char> cubin;
+    if (!get_cubin(p->source, cubin, nullptr)) { cudaSetDevice(prev); delete p; return SYMCON_ECUDA; }
+    s = cuda_err(cudaLibraryLoadData(&p->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0), "cudaLibraryLoadData");
+    if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_fold, p->lib, "symcon_fold"), "get symcon_fold");
+    if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_fwd, p->lib, "symcon_fwd"), "get symcon_fwd");
+    if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_dA, p->lib, "symcon_bwd_dA"), "get symcon_bwd_dA");
+    if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_dW, p->lib, "symcon_bwd_dW"), "get symcon_bwd_dW");
+    if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_unfold, p->lib, "symcon_unfold"), "get symcon_unfold");
+    cudaSetDevice(prev);
+    if (s) { if (p->lib) cudaLibraryUnload(p->lib); delete p; return s; }
+  }
+  *plan = p;
+  return SYMCON_OK;
+}
+
+/* Compile (NVRTC, sm_100a) the kernels for a configuration into the cubin cache without a
+ * device (used by the build step on CPU-only hosts). Writes the cubin path if path != NULL. */
+symcon_status symcon_precompile(int lmax_in, int correlation, const int* out_L, int n_out, char* path, size_t path_len) {
+  symcon_plan* p = nullptr;
+  symcon_status s = build_common(lmax_in, correlation, out_L, n_out, 1, 1, &p);
+  if (s) return s;
+  std::vector<char> cubin;
+  std::string cp;
+  bool ok = get_cubin(p->source, cubin, &cp);
+  delete p;
+  if (!ok) return SYMCON_ECUDA;
+  if (path && path_len) { strncpy(path, cp.c_str(), path_len - 1); path[path_len - 1] = 0; }
+  return SYMCON_OK;
+}
+
+/* Copy the generated CUDA source of a plan (NULL buf: returns the needed size incl. NUL). */
+size_t symcon_plan_source(const symcon_plan* p, char* buf, size_t len) {
+  if (!p) return 0;
+  if (!buf) return p->source.size() + 1;
+  size_t n = std::min(len - 1, p->source.size());
+  memcpy(buf, p->source.data(), n);
+  buf[n] = 0;
+  return n + 1;
+}
+
+symcon_status symcon_plan_info(const symcon_plan* p, symcon_info* info) {
+  if (!p || !info) { set_error("NULL argument"); return SYMCON_EINVAL; }
+  memset(info, 0, sizeof *info);
+  const Tables& t = p->t;
+  info->lmax_in = t.lmax_in;
+  info->correlation = t.corr;
+  info->n_out = (int)t.out_L.size();
+  info->num_elements = t.E;
+  info->channels = t.K;
+  for (size_t i = 0; i < t.out_L.size(); i++) info->out_L[i] = t.out_L[i];
+  for (auto& pd : t.paths) {
+    int oi = (int)(std::find(t.out_L.begin(), t.out_L.end(), pd.L) - t.out_L.begin());
+    info->eta[oi][pd.nu - 1]++;
+  }
+  info->n_paths = (int64_t)t.paths.size();
+  info->weight_numel = (int64_t)t.E * info->n_paths * t.K;
+  info->in_dim = (int64_t)t.K * t.n_lm;
+  info->out_dim = (int64_t)t.K * t.out_per_ch;
+  info->n_raw_terms = t.n_raw_terms;
+  info->n_sym_terms = t.n_sym_terms;
+  info->n_fold = (int64_t)t.rows.size();
+  info->n_monomials = t.n_monomials;
+  info->device = p->device;
+  return SYMCON_OK;
+}
+
+symcon_status symcon_plan_path(const symcon_plan* p, int64_t col, int32_t* L, int32_t* nu, int32_t* eta,
+                               int32_t* ls, int32_t* mids) {
+  if (!p || col < 0 || col >= (int64_t)p->t.paths.size()) { set_error("bad column"); return SYMCON_EINVAL; }
+  const PathDesc& d = p->t.paths[col];
+  if (L) *L = d.L;
+  if (nu) *nu = d.nu;
+  if (eta) *eta = d.eta;
+  if (ls) for (int j = 0; j < d.nu; j++) ls[j] = d.ls[j];
+  if (mids) for (int j = 0; j + 1 < d.nu; j++) mids[j] = d.mids[j];
+  return SYMCON_OK;
+}
+
+symcon_status symcon_plan_sym_table(const symcon_plan* p, int64_t* n, int32_t* L, int32_t* M, int32_t* mono3,
+                                    int32_t* col, double* value) {
+  if (!p || !n) { set_error("NULL argument"); return SYMCON_EINVAL; }
+  if (!L && !M && !mono3 && !col && !value) { *n = p->t.n_sym_terms; return SYMCON_OK; }
+  if (*n < p->t.n_sym_terms) { *n = p->t.n_sym_terms; set_error("arrays too small"); return SYMCON_ENOMEM; }
+  int64_t q = 0;
+  for (auto& r : p->t.rows)
+    for (auto& cv : r.cols) {
+      if (L) L[q] = r.L;
+      if (M) M[q] = r.M;
+      if (mono3) for (int j = 0; j < 3; j++) mono3[3 * q + j] = r.mono[j];
+      if (col) col[q] = cv.first;
+      if (value) value[q] = cv.second;
+      q++;
+    }
+  *n = q;
+  return SYMCON_OK;
+}
+
+size_t symcon_workspace_bytes(const symcon_plan* p, int64_t N) {
+  if (!p || N < 0) return 0;
+  return layout(p, N).total;
+}
+
+int32_t symcon_last_launch_count(const symcon_plan* p) { return p ? p->last_launches.load() : 0; }
+
+static symcon_status check_common(const symcon_plan* p, int64_t N, const float* A, const float* W, const int32_t* ne,
+                                  void* ws, size_t ws_bytes) {
+  if (!p) { set_error("plan is NULL"); return SYMCON_EINVAL; }
+  if (p->device < 0 || !p->lib) { set_error("host-only plan: no kernels loaded"); return SYMCON_EINVAL; }
+  if (N < 0 || N > (int64_t)0x7fffffff) { set_error("num_nodes out of range"); return SYMCON_EINVAL; }
+  if (N == 0) return SYMCON_OK;
+  if (!A || !W || !ne || !ws) { set_error("NULL device pointer"); return SYMCON_EINVAL; }
+  if (!aligned16(A) || !aligned16(ws)) { set_error("A and workspace must be 16-byte aligned"); return SYMCON_EINVAL; }
+  if (ws_bytes < layout(p, N).total) { set_error("workspace too small"); return SYMCON_ENOMEM; }
+  return SYMCON_OK;
+}
+
+static void fill_params(const symcon_plan* p, const WsLayout& w, char* ws, int64_t N, Params& q) {
+  memset(&q, 0, sizeof q);
+  q.perm = (const int*)(ws + w.perm);
+  q.tiles = (const int4*)(ws + w.tiles);
+  q.n_tiles = (const int*)(ws + w.n_tiles);
+  q.items = (const int4*)(ws + w.items);
+  q.n_items = (const int*)(ws + w.n_items);
+  q.item_off = (const int*)(ws + w.item_off);
+  q.seg_off = (const int*)(ws + w.seg_off);
+  q.coef = (float*)(ws + w.coef);
+  q.spart = (float*)(ws + w.spart);
+  q.N = (int)N;
+  q.K = p->t.K;
+  q.E = p->t.E;
+}
+
+static int launch_prep(const symcon_plan* p, const WsLayout& w, char* ws, int64_t N, const int32_t* ne, const float* W,
+                       Params& q, cudaStream_t st, bool fold, symcon_status* s) {
+  int n = 0;
+  BucketArgs b;
+  b.node_elem = ne;
+  b.N = (int)N;
+  b.E = p->t.E;
+  b.tile_nodes = p->kc.tile_nodes;
+  b.tiles_per_item = p->kc.dw_tiles_per_item;
+  b.hist = (int*)(ws + w.hist);
+  b.off = (int*)(ws + w.off);
+  b.seg_off = (int*)(ws + w.seg_off);
+  b.perm = (int*)(ws + w.perm);
+  b.tiles = (int4*)(ws + w.tiles);
+  b.n_tiles = (int*)(ws + w.n_tiles);
+  b.items = (int4*)(ws + w.items);
+  b.n_items = (int*)(ws + w.n_items);
+  b.item_off = (int*)(ws + w.item_off);
+  b.err = (unsigned long long*)(ws + w.err);
+  {
+    Timed tm(p, K_BUCKET, st);
+    n += bucket_launch(b, st);
+  }
+  if (fold) {
+    Timed tm(p, K_FOLD, st);
+    q.W = W;
+    void* args[] = {&q};
+    dim3 grid(p->t.E, (p->t.K + 31) / 32);
+    *s = cuda_err(cudaLaunchKernel((const void*)p->k_fold, grid, dim3(32), args, 0, st), "launch symcon_fold");
+    n++;
+  }
+  return n;
+}
+
+symcon_status symcon_forward(const symcon_plan* p, int64_t N, const float* A, const float* W, const int32_t* ne,
+                             float* B, void* ws, size_t ws_bytes, void* stream) {
+  symcon_status s = check_common(p, N, A, W, ne, ws, ws_bytes);
+  if (s) return s;
+  p->last_launches = 0;
+  if (N == 0) return SYMCON_OK;
+  if (!B || !aligned16(B)) { set_error("B must be non-NULL and 16-byte aligned"); return SYMCON_EINVAL; }
+  cudaStream_t st = (cudaStream_t)stream;
+  WsLayout w = layout(p, N);
+  Params q;
+  fill_params(p, w, (char*)ws, N, q);
+  q.A = A;
+  q.W = W;
+  q.node_elem = ne;
+  q.B = B;
+  int n = launch_prep(p, w, (char*)ws, N, ne, W, q, st, true, &s);
+  if (s) return s;
+  void* args[] = {&q};
+  dim3 grid((unsigned)w.max_tiles, (p->t.K + p->kc.warps_per_cta - 1) / p->kc.warps_per_cta);
+  {
+    Timed tm(p, K_FWD, st);
+    s = cuda_err(cudaLaunchKernel((const void*)p->k_fwd, grid, dim3(32 * p->kc.warps_per_cta), args, 0, st), "launch symcon_fwd");
+  }
+  n++;
+  if (s) return s;
+  Timed tn(p, K_NAN, st);
+  n += fill_nan_launch(q.perm, q.seg_off, p->t.E, B, (long long)p->t.K * p->t.out_per_ch, st);
+  p->last_launches = n;
+  return cuda_err(cudaGetLastError(), "forward launch");
+}
+
+symcon_status symcon_backward(const symcon_plan* p, int64_t N, const float* A, const float* W, const int32_t* ne,
+                              const float* dB, float* dA, float* dW, void* ws, size_t ws_bytes, void* stream) {
+  if (!p) { set_error("plan is NULL"); return SYMCON_EINVAL; }
+  cudaStream_t st = (cudaStream_t)stream;
+  p->last_launches = 0;
+  if (N == 0) {
+    // no nodes: dW must still be overwritten with zeros (reading s12)
+    if (dW) return cuda_err(cudaMemsetAsync(dW, 0, sizeof(float) * (size_t)p->t.E * p->t.paths.size() * p->t.K, st), "memset dW");
+    return SYMCON_OK;
+  }
+  symcon_status s = check_common(p, N, A, W, ne, ws, ws_bytes);
+  if (s) return s;
+  if (!dB || !aligned16(dB)) { set_error("dB must be non-NULL and 16-byte aligned"); return SYMCON_EINVAL; }
+  if (dA && !aligned16(dA)) { set_error("dA must be 16-byte aligned"); return SYMCON_EINVAL; }
+  if (!dA && !dW) return SYMCON_OK;
+  WsLayout w = layout(p, N);
+  Params q;
+  fill_params(p, w, (char*)ws, N, q);
+  q.A = A;
+  q.W = W;
+  q.node_elem = ne;
+  q.dB = dB;
+  q.dA = dA;
+  q.dW = dW;
+  int n = launch_prep(p, w, (char*)ws, N, ne, W, q, st, dA != nullptr, &s);
+  if (s) return s;
+  void* args[] = {&q};
+  const unsigned ky = (p->t.K + p->kc.warps_per_cta - 1) / p->kc.warps_per_cta;
+  if (dW) {
+    {
+    Timed tm(p, K_DW, st);
+    s = cuda_err(cudaLaunchKernel((const void*)p->k_dW, dim3((unsigned)w.max_items, ky), dim3(32 * p->kc.warps_per_cta),
+                                  args, 0, st), "launch symcon_bwd_dW");
+    }
+    if (s) return s;
+    Timed tm(p, K_UNFOLD, st);
+    s = cuda_err(cudaLaunchKernel((const void*)p->k_unfold, dim3(p->t.E, (p->t.K + p->kc.unfold_channels - 1) / p->kc.unfold_channels),
+                                  dim3(32), args, 0, st), "launch symcon_unfold");
+    if (s) return s;
+    n += 2;
+  }
+  if (dA) {
+    {
+    Timed tm(p, K_DA, st);
+    s = cuda_err(cudaLaunchKernel((const void*)p->k_dA, dim3((unsigned)w.max_tiles, ky), dim3(32 * p->kc.warps_per_cta),
+                                  args, 0, st), "launch symcon_bwd_dA");
+    }
+    if (s) return s;
+    n++;
+    Timed tn(p, K_NAN, st);
+    n += fill_nan_launch(q.perm, q.seg_off, p->t.E, dA, (long long)p->t.K * p->t.n_lm, st);
+  }
+  p->last_launches = n;
+  return cuda_err(cudaGetLastError(), "backward launch");
+}
+
+symcon_status symcon_check_device_error(const symcon_plan* p, void* ws, void* stream, int64_t* first_bad) {
+  if (!p || !ws) { set_error("NULL argument"); return SYMCON_EINVAL; }
+  cudaStream_t st = (cudaStream_t)stream;
+  symcon_status s = cuda_err(cudaStreamSynchronize(st), "stream sync");
+  if (s) return s;
+  WsLayout w = layout(p, 0);
+  unsigned long long e = 0;
+  s = cuda_err(cudaMemcpy(&e, (char*)ws + w.err, sizeof e, cudaMemcpyDeviceToHost), "read error word");
+  if (s) return s;
+  if (e != ~0ull) {
+    if (first_bad) *first_bad = (int64_t)e;
+    set_error("node_elem out of range at node " + std::to_string(e));
+    return SYMCON_EELEMENT;
+  }
+  if (first_bad) *first_bad = -1;
+  return SYMCON_OK;
+}
+
+/* Launch timer: when on, each launch group is bracketed by CUDA events on its stream. */
+symcon_status symcon_profile_enable(const symcon_plan* p, int on) {
+  if (!p) return SYMCON_EINVAL;
+  p->prof_on = on != 0;
+  return SYMCON_OK;
+}
+
+symcon_status symcon_profile_reset(const symcon_plan* p) {
+  if (!p) return SYMCON_EINVAL;
+  std::lock_guard<std::mutex> g(p->prof_mu);
+  drain(p);
+  for (int i = 0; i < 8; i++) { p->prof_ms[i] = 0; p->prof_n[i] = 0; }
+  return SYMCON_OK;
+}
+
+/* Synchronises the recorded events; fills up to 8 (name, launches, total ms) entries. */
+int32_t symcon_profile_read(const symcon_plan* p, const char** names, int64_t* counts, double* total_ms) {
+  if (!p) return 0;
+  std::lock_guard<std::mutex> g(p->prof_mu);
+  drain(p);
+  int n = 0;
+  for (int i = 0; i < 8; i++)
+    if (p->prof_n[i]) {
+      if (names) names[n] = kKindNames[i];
+      if (counts) counts[n] = p->prof_n[i];
+      if (total_ms) total_ms[n] = p->prof_ms[i];
+      n++;
+    }
+  return n;
+}
+
+void symcon_destroy(symcon_plan* p) {
+  if (!p) return;
+  {
+    std::lock_guard<std::mutex> g(p->prof_mu);
+    for (auto& r : p->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : p->event_pool) cudaEventDestroy(e);
+  }
+  if (p->lib) cudaLibraryUnload(p->lib);
+  delete p;
+}
+
+symcon_status symcon_pack_balanced(const int64_t* sizes, int64_t n, int64_t C, int32_t G, int64_t* bin_offsets,
+                                   int64_t* graph_ids, int64_t max_bins, int64_t* n_bins) {
+  if (!n_bins || (n > 0 && !sizes) || C < 1 || G < 1 || n < 0) { set_error("bad argument"); return SYMCON_EINVAL; }
+  for (int64_t i = 0; i < n; i++)
+    if (sizes[i] > C || sizes[i] < 0) { set_error("graph " + std::to_string(i) + " larger than capacity"); return SYMCON_EINVAL; }
+  std::vector<std::vector<int64_t>> bins;
+  pack_balanced(sizes, n, C, G, bins);
+  *n_bins = (int64_t)bins.size();
+  if ((int64_t)bins.size() > max_bins || !bin_offsets || (n > 0 && !graph_ids)) { set_error("max_bins too small"); return SYMCON_ENOMEM; }
+  int64_t o = 0;
+  for (size_t b = 0; b < bins.size(); b++) {
+    bin_offsets[b] = o;
+    for (int64_t g : bins[b]) graph_ids[o++] = g;
+  }
+  bin_offsets[bins.size()] = o;
+  return SYMCON_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,153 @@
+// Element bucketing: a stable counting sort of nodes by element so
+// that every 64-node tile of the contraction kernels belongs to ONE element (W depends on
+// z_i) and its per-(element, channel) coefficients are warp-uniform.
+//
+//   bk_hist     per 1024-node chunk: histogram over E+1 buckets (bucket E = out-of-range
+//               node_elem; the first such node index is recorded in *err)
+//   bk_scan     one CTA: chunk offsets (element-major), seg_off, the tile list (<= 64 nodes,
+//               one element each) and the dW item list (<= R tiles of one element each)
+//   bk_scatter  one warp per chunk, 32 nodes at a time with __match_any_sync ranks: stable
+//   bk_fill_nan writes NaN rows for nodes in the out-of-range bucket
+// All integer work; deterministic for a given node_elem.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kernels.h"
+
+namespace symcon {
+
+static constexpr int kChunk = 1024;
+
+__global__ void bk_hist(const int* __restrict__ ne, int N, int E, int* __restrict__ hist,
+                        unsigned long long* err) {
+  extern __shared__ int h[];
+  for (int e = threadIdx.x; e <= E; e += blockDim.x) h[e] = 0;
+  __syncthreads();
+  const int base = blockIdx.x * kChunk;
+  for (int t = threadIdx.x; t < kChunk; t += blockDim.x) {
+    int i = base + t;
+    if (i >= N) break;
+    int e = ne[i];
+    if (e < 0 || e >= E) {
+      e = E;
+      atomicMin(err, (unsigned long long)i);
+    }
+    atomicAdd(&h[e], 1);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e <= E; e += blockDim.x) hist[(size_t)blockIdx.x * (E + 1) + e] = h[e];
+}
+
+__global__ void bk_scan(const int* __restrict__ hist, int nchunks, int E, int* __restrict__ off,
+                        int* __restrict__ seg_off, int4* __restrict__ tiles, int* __restrict__ n_tiles,
+                        int4* __restrict__ items, int* __restrict__ n_items, int* __restrict__ item_off,
+                        int tile_nodes, int tiles_per_item) {
+  extern __shared__ int sm[];   // tot[E+1], tile_off[E+1], itm_off[E+1]
+  int* tot = sm;
+  int* toff = sm + (E + 1);
+  int* ioff = sm + 2 * (E + 1);
+  for (int e = threadIdx.x; e <= E; e += blockDim.x) {
+    int s = 0;
+    for (int c = 0; c < nchunks; c++) s += hist[(size_t)c * (E + 1) + e];
+    tot[e] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0, ts = 0, is = 0;
+    for (int e = 0; e <= E; e++) {
+      int c = tot[e];
+      tot[e] = s;          // becomes the segment start
+      seg_off[e] = s;
+      s += c;
+      int nt = (e < E) ? (c + tile_nodes - 1) / tile_nodes : 0;
+      toff[e] = ts;
+      ts += nt;
+      int ni = (nt + tiles_per_item - 1) / tiles_per_item;
+      ioff[e] = is;
+      item_off[e] = is;
+      is += ni;
+    }
+    seg_off[E + 1] = s;
+    *n_tiles = ts;
+    *n_items = is;
+    item_off[E + 1] = is;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e <= E; e += blockDim.x) {
+    int r = tot[e];
+    for (int c = 0; c < nchunks; c++) {
+      off[(size_t)c * (E + 1) + e] = r;
+      r += hist[(size_t)c * (E + 1) + e];
+    }
+    if (e < E) {
+      const int start = tot[e], cnt = r - tot[e];
+      const int nt = (cnt + tile_nodes - 1) / tile_nodes;
+      for (int t = 0; t < nt; t++) {
+        int c0 = t * tile_nodes;
+        int c = min(tile_nodes, cnt - c0);
+        tiles[toff[e] + t] = make_int4(e, start + c0, c, t);
+      }
+      const int ni = (nt + tiles_per_item - 1) / tiles_per_item;
+      for (int q = 0; q < ni; q++) {
+        int t0 = q * tiles_per_item;
+        items[ioff[e] + q] = make_int4(e, toff[e] + t0, min(tiles_per_item, nt - t0), q);
+      }
+    }
+  }
+}
+
+__global__ void bk_scatter(const int* __restrict__ ne, int N, int E, const int* __restrict__ off,
+                           int* __restrict__ perm) {
+  extern __shared__ int cnt[];
+  const int lane = threadIdx.x;
+  for (int e = lane; e <= E; e += 32) cnt[e] = off[(size_t)blockIdx.x * (E + 1) + e];
+  __syncwarp();
+  const int base = blockIdx.x * kChunk;
+  for (int g = 0; g < kChunk; g += 32) {
+    const int i = base + g + lane;
+    int e = -1;
+    if (i < N) {
+      e = ne[i];
+      if (e < 0 || e >= E) e = E;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    const int leader = __ffs(peers) - 1;
+    int pos = 0;
+    if (e >= 0) pos = cnt[e] + rank;
+    __syncwarp();
+    if (e >= 0 && lane == leader) cnt[e] += __popc(peers);
+    __syncwarp();
+    if (e >= 0) perm[pos] = i;
+  }
+}
+
+__global__ void bk_fill_nan(const int* __restrict__ perm, const int* __restrict__ seg_off, int E,
+                            float* __restrict__ out, long long row) {
+  const int s = seg_off[E], t = seg_off[E + 1];
+  const float nan = __int_as_float(0x7fc00000);
+  for (int q = s + blockIdx.x; q < t; q += gridDim.x) {
+    float* r = out + (long long)perm[q] * row;
+    for (long long x = threadIdx.x; x < row; x += blockDim.x) r[x] = nan;
+  }
+}
+
+int bucket_launch(const BucketArgs& a, cudaStream_t st) {
+  const int nchunks = (a.N + kChunk - 1) / kChunk;
+  const size_t sm_e = sizeof(int) * (a.E + 1);
+  cudaMemsetAsync(a.err, 0xff, sizeof(unsigned long long), st);
+  if (a.N > 0) bk_hist<<<nchunks, 256, sm_e, st>>>(a.node_elem, a.N, a.E, a.hist, a.err);
+  bk_scan<<<1, 256, 3 * sm_e, st>>>(a.hist, nchunks, a.E, a.off, a.seg_off, a.tiles, a.n_tiles, a.items,
+                                    a.n_items, a.item_off, a.tile_nodes, a.tiles_per_item);
+  if (a.N > 0) bk_scatter<<<nchunks, 32, sm_e, st>>>(a.node_elem, a.N, a.E, a.off, a.perm);
+  return a.N > 0 ? 3 : 1;
+}
+
+int fill_nan_launch(const int* perm, const int* seg_off, int E, float* out, long long row, cudaStream_t st) {
+  bk_fill_nan<<<64, 128, 0, st>>>(perm, seg_off, E, out, row);
+  return 1;
+}
+
+size_t bucket_chunks(int64_t N) { return (size_t)((N + kChunk - 1) / kChunk); }
+
+}  // namespace symcon

@@ -1,0 +1,59 @@
+// Internal structures of libsymcon (product side; shares nothing with oracle/).
+#pragma once
+#include <array>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/symcon.h"
+
+namespace symcon {
+
+void set_error(const std::string& msg);
+
+// ---- cg.cpp: pairwise real coupling (ladder-operator construction)
+// returns [(2L+1)][(2l1+1)][(2l2+1)] row-major; zeros if the triangle rule fails.
+std::vector<double> real_coupling(int l1, int l2, int L);
+
+// ---- builder.cpp
+struct PathDesc {
+  int L, nu, eta, col;
+  std::array<int, 3> ls{{-1, -1, -1}};
+  std::array<int, 2> mids{{-1, -1}};
+};
+
+struct SymRow {                 // one (L, M, monomial) row of the symmetrised table
+  int L, M;                     // output irrep and component (M in [-L, L])
+  int out;                      // per-channel output slot: off_L + M + L
+  std::array<int, 3> mono;      // a <= b <= c, padded with -1
+  int deg;
+  std::vector<std::pair<int, double>> cols;  // (path column, U~ value)
+};
+
+struct Tables {
+  int lmax_in, corr, n_lm, E, K;
+  std::vector<int> out_L, out_off;   // out_off[i] = sum_{j<i} (2 out_L[j] + 1)
+  int out_per_ch;
+  std::vector<PathDesc> paths;
+  int64_t n_raw_terms = 0;
+  std::vector<SymRow> rows;          // in codegen order (j index)
+  int64_t n_sym_terms = 0;
+  int n_monomials = 0;
+};
+
+bool build_tables(int lmax_in, int corr, const std::vector<int>& out_L, int E, int K, Tables& t);
+
+// ---- codegen.cpp
+struct KernelConfig {
+  int warps_per_cta = 8;     // channels per CTA (one warp per channel)
+  int tile_nodes = 64;       // nodes per tile: 2 per lane
+  int dw_tiles_per_item = 8; // tiles per dW work item
+  int unfold_channels = 8;   // channels per unfold CTA
+};
+std::string generate_source(const Tables& t, const KernelConfig& kc);
+
+// ---- pack.cpp
+int64_t pack_balanced(const int64_t* sizes, int64_t n, int64_t C, int G,
+                      std::vector<std::vector<int64_t>>& bins);
+
+}  // namespace symcon

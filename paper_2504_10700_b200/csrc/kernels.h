@@ -1,0 +1,27 @@
+// Launch wrappers of the statically compiled (nvcc) kernels of libsymcon.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace symcon {
+
+struct BucketArgs {
+  const int* node_elem;
+  int N, E, tile_nodes, tiles_per_item;
+  int* hist;      // [nchunks][E+1]
+  int* off;       // [nchunks][E+1]
+  int* seg_off;   // [E+2]
+  int* perm;      // [N]
+  int4* tiles;    // [max_tiles]
+  int* n_tiles;
+  int4* items;    // [max_items]
+  int* n_items;
+  int* item_off;  // [E+2]
+  unsigned long long* err;
+};
+
+int bucket_launch(const BucketArgs& a, cudaStream_t st);   // returns launches issued
+int fill_nan_launch(const int* perm, const int* seg_off, int E, float* out, long long row, cudaStream_t st);
+size_t bucket_chunks(int64_t N);
+
+}  // namespace symcon

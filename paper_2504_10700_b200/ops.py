@@ -1,0 +1,119 @@
+"""PyTorch glue for libsymcon: device memory, streams and autograd. No compute here.
+
+    sc = SymmetricContraction(lmax_in=3, correlation=3, out_L=(0, 1), num_elements=89,
+                              channels=128, device=0)
+    B = sc(A, W, node_elem)          # autograd-aware; backward gives dA and dW
+
+Every numeric step (bucketing, W-fold, forward, dA, dW, reductions) runs in the CUDA
+kernels of libsymcon.so through the C ABI; tensors only provide pointers.
+"""
+import torch
+
+from . import _lib
+
+
+def _stream_ptr(device):
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class SymmetricContraction:
+    """One plan (U tables + loaded sm_100a kernels) per (config, device)."""
+
+    def __init__(self, lmax_in, correlation, out_L, num_elements, channels, device=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("SymmetricContraction needs a CUDA device (libsymcon has no CPU path)")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
+        self.lmax_in, self.correlation, self.out_L = lmax_in, correlation, tuple(out_L)
+        self.num_elements, self.channels = num_elements, channels
+        with torch.cuda.device(self.device):
+            self.plan = _lib.symcon_build_tables(lmax_in, correlation, list(out_L), num_elements, channels,
+                                                 self.device.index)
+        info = _lib.symcon_plan_info(self.plan)
+        self.info = info
+        self.n_paths = info.n_paths
+        self.n_lm = (lmax_in + 1) ** 2
+        self.out_dim = info.out_dim
+        self._ws = {}
+
+    def __del__(self):
+        plan = getattr(self, "plan", None)
+        if plan is not None:
+            _lib.symcon_destroy(plan)
+            self.plan = None
+
+    # ------------------------------------------------------------------ helpers
+    def block_sizes(self):
+        """[(L, nu, n_eta)] in W column order."""
+        out = []
+        for L in range(self.info.n_out):
+            for nu in range(self.correlation):
+                n = self.info.eta[L][nu]
+                if n:
+                    out.append((self.info.out_L[L], nu + 1, n))
+        return out
+
+    def workspace(self, num_nodes, key="default"):
+        nbytes = _lib.symcon_workspace_bytes(self.plan, num_nodes)
+        ws = self._ws.get(key)
+        if ws is None or ws.numel() < nbytes:
+            ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+            self._ws[key] = ws
+        return ws
+
+    def _check(self, A, W, node_elem):
+        N = A.shape[0]
+        assert A.is_cuda and A.device == self.device and A.dtype == torch.float32 and A.is_contiguous()
+        assert A.shape == (N, self.channels, self.n_lm), A.shape
+        assert W.dtype == torch.float32 and W.is_contiguous() and W.shape == (self.num_elements, self.n_paths, self.channels)
+        assert node_elem.dtype == torch.int32 and node_elem.is_contiguous() and node_elem.shape == (N,)
+        return N
+
+    # ------------------------------------------------------------------ raw calls
+    def forward_raw(self, A, W, node_elem, B=None, ws_key="default"):
+        N = self._check(A, W, node_elem)
+        if B is None:
+            B = torch.empty((N, self.out_dim), dtype=torch.float32, device=self.device)
+        ws = self.workspace(N, ws_key)
+        _lib.symcon_forward(self.plan, N, A.data_ptr(), W.data_ptr(), node_elem.data_ptr(), B.data_ptr(),
+                            ws.data_ptr(), ws.numel(), _stream_ptr(self.device))
+        return B
+
+    def backward_raw(self, A, W, node_elem, dB, need_dA=True, need_dW=True, dA=None, dW=None, ws_key="default"):
+        N = self._check(A, W, node_elem)
+        assert dB.dtype == torch.float32 and dB.is_contiguous() and dB.shape == (N, self.out_dim)
+        if need_dA and dA is None:
+            dA = torch.empty_like(A)
+        if need_dW and dW is None:
+            dW = torch.empty_like(W)
+        ws = self.workspace(N, ws_key)
+        _lib.symcon_backward(self.plan, N, A.data_ptr(), W.data_ptr(), node_elem.data_ptr(), dB.data_ptr(),
+                             dA.data_ptr() if need_dA else None, dW.data_ptr() if need_dW else None,
+                             ws.data_ptr(), ws.numel(), _stream_ptr(self.device))
+        return (dA if need_dA else None), (dW if need_dW else None)
+
+    def check_device_error(self, ws_key="default"):
+        ws = self._ws.get(ws_key)
+        if ws is None:
+            return 0, -1
+        return _lib.symcon_check_device_error(self.plan, ws.data_ptr(), _stream_ptr(self.device))
+
+    def last_launch_count(self):
+        return _lib.symcon_last_launch_count(self.plan)
+
+    # ------------------------------------------------------------------ autograd
+    def __call__(self, A, W, node_elem):
+        return _SymconFn.apply(A, W, node_elem, self)
+
+
+class _SymconFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, A, W, node_elem, sc):
+        ctx.sc = sc
+        ctx.save_for_backward(A, W, node_elem)
+        return sc.forward_raw(A.contiguous(), W.contiguous(), node_elem.contiguous())
+
+    @staticmethod
+    def backward(ctx, dB):
+        A, W, node_elem = ctx.saved_tensors
+        dA, dW = ctx.sc.backward_raw(A, W, node_elem, dB.contiguous(), ctx.needs_input_grad[0], ctx.needs_input_grad[1])
+        return dA, dW, None, None

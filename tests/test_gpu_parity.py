@@ -1,0 +1,206 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle, element by element.
+
+Tolerance: max|err| <= 1e-4 * max|ref| per tensor (north_star); internal gate 1e-5 (DESIGN.md
+§7: fp32 rounding measured <= 4e-6 of max|ref|, so an error near 1e-4 is a bug).
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+def _sc(lmax, corr, outs, E, K):
+    from paper_2504_10700_b200.ops import SymmetricContraction
+    return SymmetricContraction(lmax, corr, outs, E, K, device=0)
+
+
+def _inputs(sc, N, dist="uniform", seed=0):
+    from synth.inputs import gen_A, gen_W, gen_node_elem, gen_dB
+    A = gen_A(N, sc.channels, sc.n_lm, "cuda", seed)
+    W = gen_W(sc.num_elements, sc.block_sizes(), sc.channels, "cuda", seed)
+    ne = gen_node_elem(N, sc.num_elements, dist, "cuda", seed)
+    dB = gen_dB(N, sc.out_dim, "cuda", seed)
+    return A, W, ne, dB
+
+
+def _rel(x, ref):
+    ref = np.asarray(ref, dtype=np.float64)
+    x = np.asarray(x, dtype=np.float64)
+    scale = np.abs(ref).max()
+    return np.abs(x - ref).max() / (scale if scale > 0 else 1.0)
+
+
+def _run(sc, A, W, ne, dB):
+    B = sc.forward_raw(A, W, ne)
+    dA, dW = sc.backward_raw(A, W, ne, dB)
+    torch.cuda.synchronize()
+    s, bad = sc.check_device_error()
+    assert s == 0, bad
+    return B, dA, dW
+
+
+def _host(*ts):
+    return [t.detach().cpu().numpy() for t in ts]
+
+
+def test_tiny_against_python_oracle():
+    from oracle.contraction import Problem, forward, backward
+    sc = _sc(3, 3, (0,), 3, 16)
+    A, W, ne, dB = _inputs(sc, 32)
+    B, dA, dW = _run(sc, A, W, ne, dB)
+    prob = Problem(3, 3, (0,))
+    hA, hW, hne, hdB = _host(A, W, ne, dB)
+    Bref = forward(prob, hA, hW, hne)
+    dAref, dWref = backward(prob, hA, hW, hne, hdB)
+    assert _rel(B.cpu(), Bref) < TOL
+    assert _rel(dA.cpu(), dAref) < TOL
+    assert _rel(dW.cpu(), dWref) < TOL
+
+
+@pytest.mark.parametrize("name,lmax,corr,outs,E,K,N,dist", [
+    ("off_small_shape", 3, 3, (0,), 10, 96, 3000, "organic"),
+    ("mp_shape", 3, 3, (0, 1), 89, 128, 3000, "zipf"),
+    ("large_shape", 3, 3, (0, 1, 2), 89, 256, 700, "zipf"),
+    ("ragged_K13", 3, 3, (0, 1), 5, 13, 777, "uniform"),
+    ("lmax2", 2, 3, (0, 1), 4, 24, 500, "uniform"),
+    ("lmax1", 1, 3, (0, 1), 3, 8, 300, "uniform"),
+    ("corr1_all_L", 3, 1, (0, 1, 2, 3), 3, 16, 300, "uniform"),
+    ("corr2", 3, 2, (0, 1), 3, 16, 300, "uniform"),
+    ("out_1o_only", 3, 3, (1,), 7, 32, 500, "zipf"),
+])
+def test_against_c_oracle(name, lmax, corr, outs, E, K, N, dist):
+    from oracle.contraction import Problem
+    from oracle.ceval import OracleC
+    sc = _sc(lmax, corr, outs, E, K)
+    A, W, ne, dB = _inputs(sc, N, dist, seed=11)
+    B, dA, dW = _run(sc, A, W, ne, dB)
+    oc = OracleC(Problem(lmax, corr, outs))
+    hA, hW, hne, hdB = _host(A, W, ne, dB)
+    Bref = oc.forward(hA, hW, hne)
+    dAref, dWref = oc.backward(hA, hW, hne, hdB)
+    assert _rel(B.cpu(), Bref) < TOL, name
+    assert _rel(dA.cpu(), dAref) < TOL, name
+    assert _rel(dW.cpu(), dWref) < TOL, name
+
+
+def test_corr1_is_linear_map_exactly():
+    sc = _sc(3, 1, (0, 1, 2, 3), 3, 16)
+    A, W, ne, dB = _inputs(sc, 200)
+    B = sc.forward_raw(A, W, ne)
+    N, K = A.shape[:2]
+    off = 0
+    for c, L in enumerate((0, 1, 2, 3)):
+        blk = B[:, off:off + K * (2 * L + 1)].reshape(N, K, 2 * L + 1)
+        expect = W[ne.long()][:, c, :].unsqueeze(-1) * A[:, :, L * L:(L + 1) ** 2]
+        assert torch.equal(blk, expect)
+        off += K * (2 * L + 1)
+
+
+def test_empty_elements_get_zero_dW_and_edge_sizes():
+    sc = _sc(3, 3, (0, 1), 6, 16)
+    for N in (1, 63, 64, 65, 129):
+        A, W, _, dB = _inputs(sc, N)
+        ne = torch.full((N,), 4, dtype=torch.int32, device="cuda")
+        ne[: N // 2] = 1
+        _, _, dW = _run(sc, A, W, ne, dB)
+        for z in (0, 2, 3, 5):
+            assert torch.count_nonzero(dW[z]) == 0
+    # N = 0: no launch, dW overwritten with zeros
+    A = torch.zeros((0, 16, 16), device="cuda")
+    W = torch.randn((6, sc.n_paths, 16), device="cuda")
+    ne = torch.zeros((0,), dtype=torch.int32, device="cuda")
+    dB = torch.zeros((0, sc.out_dim), device="cuda")
+    B = sc.forward_raw(A, W, ne)
+    dW = torch.full_like(W, 7.0)
+    sc.backward_raw(A, W, ne, dB, need_dA=False, dW=dW)
+    torch.cuda.synchronize()
+    assert B.shape == (0, sc.out_dim) and torch.count_nonzero(dW) == 0
+
+
+def test_bad_element_is_reported_and_nan():
+    sc = _sc(3, 3, (0,), 3, 8)
+    A, W, ne, dB = _inputs(sc, 100)
+    ne[17] = 3
+    ne[40] = -1
+    B = sc.forward_raw(A, W, ne)
+    torch.cuda.synchronize()
+    s, bad = sc.check_device_error()
+    from paper_2504_10700_b200 import _lib
+    assert s == _lib.SYMCON_EELEMENT and bad == 17
+    assert torch.isnan(B[17]).all() and torch.isnan(B[40]).all()
+    good = torch.ones(100, dtype=torch.bool)
+    good[[17, 40]] = False
+    assert torch.isfinite(B[good.cuda()]).all()
+
+
+def test_deterministic_bitwise():
+    sc = _sc(3, 3, (0, 1), 89, 64)
+    A, W, ne, dB = _inputs(sc, 5000, "zipf")
+    r1 = _run(sc, A, W, ne, dB)
+    r2 = _run(sc, A, W, ne, dB)
+    for a, b in zip(r1, r2):
+        assert torch.equal(a, b)
+
+
+def test_identities_on_gpu_outputs():
+    """Oracle-free checks on fp32 outputs: <W,dW> = <dB,B> and the Euler identity."""
+    sc = _sc(3, 3, (0, 1), 89, 128)
+    A, W, ne, dB = _inputs(sc, 4000, "zipf")
+    B, dA, dW = _run(sc, A, W, ne, dB)
+    lhs = (W.double() * dW.double()).sum().item()
+    rhs = (dB.double() * B.double()).sum().item()
+    assert abs(lhs - rhs) <= 1e-5 * (dB.double().abs() * B.double().abs()).sum().item()
+    # Euler: sum_a A_a dA_a = sum_nu nu <dB, B_nu>; build B_nu by masking W columns
+    e = (A.double() * dA.double()).sum()
+    r = 0.0
+    for nu in (1, 2, 3):
+        Wn = W.clone()
+        col = 0
+        for (L, n, cnt) in sc.block_sizes():
+            if n != nu:
+                Wn[:, col:col + cnt] = 0
+            col += cnt
+        Bn = sc.forward_raw(A, Wn, ne)
+        r += nu * (dB.double() * Bn.double()).sum()
+    torch.cuda.synchronize()
+    assert abs(e - r).item() <= 1e-5 * abs(r).item() + 1e-3
+
+
+def test_full_size_mp_sampled():
+    """MP-medium at full size (N=50k, the bench launch config): sampled nodes vs the oracle for
+    B and dA; dW checked exactly on the three smallest elements (all their nodes)."""
+    from oracle.contraction import Problem
+    from oracle.ceval import OracleC
+    from synth.inputs import CONFIGS
+    cfg = CONFIGS["mp_medium"]
+    sc = _sc(3, 3, cfg.out_L, cfg.n_elements, cfg.channels)
+    A, W, ne, dB = _inputs(sc, cfg.n_nodes, cfg.elem_dist, seed=0)
+    B, dA, dW = _run(sc, A, W, ne, dB)
+    oc = OracleC(Problem(3, 3, cfg.out_L))
+    rng = np.random.default_rng(123)
+    idx = torch.tensor(np.sort(rng.choice(cfg.n_nodes, 96, replace=False)), device="cuda")
+    hA, hW, hne, hdB = _host(A[idx], W, ne[idx], dB[idx])
+    assert _rel(B[idx].cpu(), oc.forward(hA, hW, hne)) < TOL
+    dAref, _ = oc.backward(hA, hW, hne, hdB, want_dW=False)
+    assert _rel(dA[idx].cpu(), dAref) < TOL
+    counts = torch.bincount(ne.long(), minlength=cfg.n_elements).cpu().numpy()
+    for z in np.argsort(counts)[:3]:
+        sel = torch.nonzero(ne == int(z)).flatten()
+        hA, hne, hdB = _host(A[sel], ne[sel], dB[sel])
+        _, dWref = oc.backward(hA, W.cpu().numpy(), hne, hdB, want_dA=False)
+        assert _rel(dW[z].cpu(), dWref[z]) < TOL
+
+
+def test_autograd_wrapper():
+    sc = _sc(3, 3, (0, 1), 4, 16)
+    A, W, ne, dB = _inputs(sc, 300)
+    A.requires_grad_(True)
+    W.requires_grad_(True)
+    B = sc(A, W, ne)
+    (B * dB).sum().backward()
+    dA, dW = sc.backward_raw(A.detach(), W.detach(), ne, dB)
+    torch.cuda.synchronize()
+    assert torch.equal(A.grad, dA) and torch.equal(W.grad, dW)
