@@ -32,6 +32,8 @@ struct symcon_plan {
   KernelConfig kc;
   int device = -1;
   int npad = 0;
+  size_t unfold_smem = 0, tile_smem = 0;
+  int grid_fwd = 0, grid_dA = 0;
   std::string source;
   cudaLibrary_t lib = nullptr;
   cudaKernel_t k_fold = nullptr, k_fwd = nullptr, k_dA = nullptr, k_dW = nullptr, k_unfold = nullptr;
@@ -96,6 +98,7 @@ struct Params {  // must match SymconParams in codegen.cpp
   const int* item_off; const int* seg_off;
   float* coef; float* spart;
   int N, K, E, pad;
+  float zero;
 };
 
 struct WsLayout {
@@ -306,6 +309,24 @@ symcon_status symcon_build_tables(int lmax_in, int correlation, const int* out_L
     if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_dA, p->lib, "symcon_bwd_dA"), "get symcon_bwd_dA");
     if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_dW, p->lib, "symcon_bwd_dW"), "get symcon_bwd_dW");
     if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_unfold, p->lib, "symcon_unfold"), "get symcon_unfold");
+    p->tile_smem = sizeof(float) * (size_t)p->kc.tile_warps * (2 * 2 * p->t.n_lm * 32 + 2 * (size_t)p->npad);
+    if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         (int)p->tile_smem, device), "fwd smem attribute");
+    if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_dA, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         (int)p->tile_smem, device), "dA smem attribute");
+    if (!s) {
+      int sms = 0, occ_f = 0, occ_a = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+      s = cuda_err(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, (const void*)p->k_fwd, 32 * p->kc.tile_warps,
+                                                                 p->tile_smem), "occupancy fwd");
+      if (!s) s = cuda_err(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, (const void*)p->k_dA, 32 * p->kc.tile_warps,
+                                                                         p->tile_smem), "occupancy dA");
+      p->grid_fwd = sms * std::max(occ_f, 1);
+      p->grid_dA = sms * std::max(occ_a, 1);
+    }
+    p->unfold_smem = sizeof(float) * 32 * (size_t)(p->npad + 1);
+    if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_unfold, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         (int)p->unfold_smem, device), "unfold smem attribute");
     cudaSetDevice(prev);
     if (s) { if (p->lib) cudaLibraryUnload(p->lib); delete p; return s; }
   }
@@ -428,6 +449,7 @@ static void fill_params(const symcon_plan* p, const WsLayout& w, char* ws, int64
   q.N = (int)N;
   q.K = p->t.K;
   q.E = p->t.E;
+  q.zero = -0.0f;
 }
 
 static int launch_prep(const symcon_plan* p, const WsLayout& w, char* ws, int64_t N, const int32_t* ne, const float* W,
@@ -482,10 +504,10 @@ symcon_status symcon_forward(const symcon_plan* p, int64_t N, const float* A, co
   int n = launch_prep(p, w, (char*)ws, N, ne, W, q, st, true, &s);
   if (s) return s;
   void* args[] = {&q};
-  dim3 grid((unsigned)w.max_tiles, (p->t.K + p->kc.warps_per_cta - 1) / p->kc.warps_per_cta);
   {
     Timed tm(p, K_FWD, st);
-    s = cuda_err(cudaLaunchKernel((const void*)p->k_fwd, grid, dim3(32 * p->kc.warps_per_cta), args, 0, st), "launch symcon_fwd");
+    s = cuda_err(cudaLaunchKernel((const void*)p->k_fwd, dim3(p->grid_fwd), dim3(32 * p->kc.tile_warps), args, p->tile_smem, st),
+                 "launch symcon_fwd");
   }
   n++;
   if (s) return s;
@@ -531,16 +553,16 @@ symcon_status symcon_backward(const symcon_plan* p, int64_t N, const float* A, c
     }
     if (s) return s;
     Timed tm(p, K_UNFOLD, st);
-    s = cuda_err(cudaLaunchKernel((const void*)p->k_unfold, dim3(p->t.E, (p->t.K + p->kc.unfold_channels - 1) / p->kc.unfold_channels),
-                                  dim3(32), args, 0, st), "launch symcon_unfold");
+    s = cuda_err(cudaLaunchKernel((const void*)p->k_unfold, dim3(p->t.E, (p->t.K + 31) / 32), dim3(256), args,
+                                  p->unfold_smem, st), "launch symcon_unfold");
     if (s) return s;
     n += 2;
   }
   if (dA) {
     {
     Timed tm(p, K_DA, st);
-    s = cuda_err(cudaLaunchKernel((const void*)p->k_dA, dim3((unsigned)w.max_tiles, ky), dim3(32 * p->kc.warps_per_cta),
-                                  args, 0, st), "launch symcon_bwd_dA");
+    s = cuda_err(cudaLaunchKernel((const void*)p->k_dA, dim3(p->grid_dA), dim3(32 * p->kc.tile_warps), args, p->tile_smem, st),
+                 "launch symcon_bwd_dA");
     }
     if (s) return s;
     n++;

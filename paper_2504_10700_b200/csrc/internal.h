@@ -45,9 +45,12 @@ bool build_tables(int lmax_in, int corr, const std::vector<int>& out_L, int E, i
 
 // ---- codegen.cpp
 struct KernelConfig {
-  int warps_per_cta = 8;     // channels per CTA (one warp per channel)
+  int warps_per_cta = 8;     // dW kernel: channels per CTA (one warp per channel)
+  int tile_warps = 4;        // fwd / dA persistent kernels: warps (channels) per CTA
   int tile_nodes = 64;       // nodes per tile: 2 per lane
   int dw_tiles_per_item = 8; // tiles per dW work item
+  int dw_tiles_per_butterfly = 2;  // tiles whose products are summed before one cross-lane reduction
+  int dw_min_blocks = 2;           // __launch_bounds__ min blocks of the dW kernel
   int unfold_channels = 8;   // channels per unfold CTA
 };
 std::string generate_source(const Tables& t, const KernelConfig& kc);
