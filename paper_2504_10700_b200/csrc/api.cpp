@@ -99,10 +99,11 @@ struct Params {  // must match SymconParams in codegen.cpp
   float* coef; float* spart;
   int N, K, E, pad;
   float zero;
+  const int* tile_perm;
 };
 
 struct WsLayout {
-  size_t hist, off, seg_off, perm, tiles, n_tiles, items, n_items, item_off, err, coef, spart, total;
+  size_t hist, off, seg_off, perm, tiles, n_tiles, items, n_items, item_off, err, coef, spart, tile_off, tile_perm, total;
   int64_t max_tiles, max_items;
 };
 
@@ -126,6 +127,8 @@ WsLayout layout(const symcon_plan* p, int64_t N) {
   w.items = take(sizeof(int4) * w.max_items);
   w.n_items = take(sizeof(int));
   w.item_off = take(sizeof(int) * (E + 2));
+  w.tile_off = take(sizeof(int) * (E + 2));
+  w.tile_perm = take(sizeof(int) * (size_t)w.max_tiles * p->kc.tile_nodes);
   w.coef = take(sizeof(float) * (size_t)E * K * p->npad);
   w.spart = take(sizeof(float) * (size_t)w.max_items * K * p->npad);
   w.total = o;
@@ -309,7 +312,7 @@ symcon_status symcon_build_tables(int lmax_in, int correlation, const int* out_L
     if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_dA, p->lib, "symcon_bwd_dA"), "get symcon_bwd_dA");
     if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_dW, p->lib, "symcon_bwd_dW"), "get symcon_bwd_dW");
     if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_unfold, p->lib, "symcon_unfold"), "get symcon_unfold");
-    p->tile_smem = sizeof(float) * (size_t)p->kc.tile_warps * (2 * 2 * p->t.n_lm * 32 + 2 * (size_t)p->npad);
+    p->tile_smem = sizeof(float) * (size_t)p->kc.tile_warps * (2 * (size_t)p->npad);
     if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                          (int)p->tile_smem, device), "fwd smem attribute");
     if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_dA, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -446,6 +449,7 @@ static void fill_params(const symcon_plan* p, const WsLayout& w, char* ws, int64
   q.seg_off = (const int*)(ws + w.seg_off);
   q.coef = (float*)(ws + w.coef);
   q.spart = (float*)(ws + w.spart);
+  q.tile_perm = (const int*)(ws + w.tile_perm);
   q.N = (int)N;
   q.K = p->t.K;
   q.E = p->t.E;
@@ -471,6 +475,9 @@ static int launch_prep(const symcon_plan* p, const WsLayout& w, char* ws, int64_
   b.n_items = (int*)(ws + w.n_items);
   b.item_off = (int*)(ws + w.item_off);
   b.err = (unsigned long long*)(ws + w.err);
+  b.tile_off = (int*)(ws + w.tile_off);
+  b.tile_perm = (int*)(ws + w.tile_perm);
+  b.max_tiles = w.max_tiles;
   {
     Timed tm(p, K_BUCKET, st);
     n += bucket_launch(b, st);
@@ -553,7 +560,7 @@ symcon_status symcon_backward(const symcon_plan* p, int64_t N, const float* A, c
     }
     if (s) return s;
     Timed tm(p, K_UNFOLD, st);
-    s = cuda_err(cudaLaunchKernel((const void*)p->k_unfold, dim3(p->t.E, (p->t.K + 31) / 32), dim3(256), args,
+    s = cuda_err(cudaLaunchKernel((const void*)p->k_unfold, dim3(p->t.E, (p->t.K + 31) / 32), dim3(512), args,
                                   p->unfold_smem, st), "launch symcon_unfold");
     if (s) return s;
     n += 2;

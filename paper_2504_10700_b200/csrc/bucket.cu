@@ -41,7 +41,7 @@ __global__ void bk_hist(const int* __restrict__ ne, int N, int E, int* __restric
 __global__ void bk_scan(const int* __restrict__ hist, int nchunks, int E, int* __restrict__ off,
                         int* __restrict__ seg_off, int4* __restrict__ tiles, int* __restrict__ n_tiles,
                         int4* __restrict__ items, int* __restrict__ n_items, int* __restrict__ item_off,
-                        int tile_nodes, int tiles_per_item) {
+                        int* __restrict__ tile_off, int tile_nodes, int tiles_per_item) {
   extern __shared__ int sm[];   // tot[E+1], tile_off[E+1], itm_off[E+1]
   int* tot = sm;
   int* toff = sm + (E + 1);
@@ -61,6 +61,7 @@ __global__ void bk_scan(const int* __restrict__ hist, int nchunks, int E, int* _
       s += c;
       int nt = (e < E) ? (c + tile_nodes - 1) / tile_nodes : 0;
       toff[e] = ts;
+      tile_off[e] = ts;
       ts += nt;
       int ni = (nt + tiles_per_item - 1) / tiles_per_item;
       ioff[e] = is;
@@ -68,6 +69,7 @@ __global__ void bk_scan(const int* __restrict__ hist, int nchunks, int E, int* _
       is += ni;
     }
     seg_off[E + 1] = s;
+    tile_off[E] = ts;
     *n_tiles = ts;
     *n_items = is;
     item_off[E + 1] = is;
@@ -97,7 +99,8 @@ __global__ void bk_scan(const int* __restrict__ hist, int nchunks, int E, int* _
 }
 
 __global__ void bk_scatter(const int* __restrict__ ne, int N, int E, const int* __restrict__ off,
-                           int* __restrict__ perm) {
+                           const int* __restrict__ seg_off, const int* __restrict__ tile_off, int tile_nodes,
+                           int* __restrict__ perm, int* __restrict__ tile_perm) {
   extern __shared__ int cnt[];
   const int lane = threadIdx.x;
   for (int e = lane; e <= E; e += 32) cnt[e] = off[(size_t)blockIdx.x * (E + 1) + e];
@@ -119,6 +122,10 @@ __global__ void bk_scatter(const int* __restrict__ ne, int N, int E, const int* 
     if (e >= 0 && lane == leader) cnt[e] += __popc(peers);
     __syncwarp();
     if (e >= 0) perm[pos] = i;
+    if (e >= 0 && e < E) {  // padded per-tile node list: tile_perm[tile][slot], -1 = empty slot
+      const int r = pos - seg_off[e];
+      tile_perm[(size_t)(tile_off[e] + r / tile_nodes) * tile_nodes + r % tile_nodes] = i;
+    }
   }
 }
 
@@ -138,8 +145,11 @@ int bucket_launch(const BucketArgs& a, cudaStream_t st) {
   cudaMemsetAsync(a.err, 0xff, sizeof(unsigned long long), st);
   if (a.N > 0) bk_hist<<<nchunks, 256, sm_e, st>>>(a.node_elem, a.N, a.E, a.hist, a.err);
   bk_scan<<<1, 256, 3 * sm_e, st>>>(a.hist, nchunks, a.E, a.off, a.seg_off, a.tiles, a.n_tiles, a.items,
-                                    a.n_items, a.item_off, a.tile_nodes, a.tiles_per_item);
-  if (a.N > 0) bk_scatter<<<nchunks, 32, sm_e, st>>>(a.node_elem, a.N, a.E, a.off, a.perm);
+                                    a.n_items, a.item_off, a.tile_off, a.tile_nodes, a.tiles_per_item);
+  cudaMemsetAsync(a.tile_perm, 0xff, sizeof(int) * (size_t)a.max_tiles * a.tile_nodes, st);
+  if (a.N > 0)
+    bk_scatter<<<nchunks, 32, sm_e, st>>>(a.node_elem, a.N, a.E, a.off, a.seg_off, a.tile_off, a.tile_nodes, a.perm,
+                                          a.tile_perm);
   return a.N > 0 ? 3 : 1;
 }
 

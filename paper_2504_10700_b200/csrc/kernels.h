@@ -17,6 +17,9 @@ struct BucketArgs {
   int4* items;    // [max_items]
   int* n_items;
   int* item_off;  // [E+2]
+  int* tile_off;  // [E+1]
+  int* tile_perm; // [max_tiles][tile_nodes], -1 padded
+  int64_t max_tiles;
   unsigned long long* err;
 };
 
