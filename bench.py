@@ -243,7 +243,7 @@ def run_ours(args):
         b, N, A, ne, dB, B, dA = pool[q % POOL]
         sc.forward_raw(A, W, ne, B=B)
         launches[0] += sc.last_launch_count()
-        sc.backward_raw(A, W, ne, dB, dA=dA, dW=dW)
+        sc.backward_raw(A, W, ne, dB, dA=dA, dW=dW, reuse=True)
         launches[0] += sc.last_launch_count()
         if world > 1:
             dist.all_reduce(dW)
@@ -293,7 +293,7 @@ def run_ours(args):
         ne2.copy_(hne, non_blocking=True)
         dB2.copy_(hdB, non_blocking=True)
         Bx = sc.forward_raw(A2, W, ne2, B=B)
-        sc.backward_raw(A2, W, ne2, dB2, dA=dA2, dW=dW)
+        sc.backward_raw(A2, W, ne2, dB2, dA=dA2, dW=dW, reuse=True)
         if world > 1:
             dist.all_reduce(dW)
         hdW.copy_(dW, non_blocking=True)

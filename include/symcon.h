@@ -111,6 +111,19 @@ symcon_status symcon_backward(const symcon_plan* plan, int64_t num_nodes, const 
                               const float* W, const int32_t* node_elem, const float* dB, float* dA,
                               float* dW, void* ws, size_t ws_bytes, void* stream /* cudaStream_t */);
 
+/* Reuse hints for symcon_backward_ex (a training step calls forward then backward with the
+ * same node_elem and W on the same workspace):
+ *   SYMCON_REUSE_BUCKETS  skip the element bucketing if the last call on `ws` used the same
+ *                         num_nodes and node_elem pointer (the caller promises unchanged contents);
+ *   SYMCON_REUSE_FOLD     additionally skip the W-fold if that call also used the same W pointer.
+ * Hints never change results: when the recorded pointers differ the work is redone. */
+#define SYMCON_REUSE_BUCKETS 1u
+#define SYMCON_REUSE_FOLD 2u
+symcon_status symcon_backward_ex(const symcon_plan* plan, int64_t num_nodes, const float* A,
+                                 const float* W, const int32_t* node_elem, const float* dB, float* dA,
+                                 float* dW, void* ws, size_t ws_bytes, uint32_t flags,
+                                 void* stream /* cudaStream_t */);
+
 /* Synchronises `stream`; returns SYMCON_EELEMENT and *first_bad_node if the last forward /
  * backward that used `ws` saw an out-of-range node_elem, SYMCON_ECUDA on a CUDA error. */
 symcon_status symcon_check_device_error(const symcon_plan* plan, void* ws, void* stream,

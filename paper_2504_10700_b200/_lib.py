@@ -20,7 +20,7 @@ lib = ctypes.CDLL(LIB_PATH)
 SYMCON_OK, SYMCON_EINVAL, SYMCON_EUNSUPPORTED, SYMCON_ECUDA, SYMCON_ENOMEM, SYMCON_EELEMENT = range(6)
 
 EXPORTS = ["symcon_build_tables", "symcon_plan_info", "symcon_plan_path", "symcon_plan_sym_table", "symcon_real_cg",
-           "symcon_workspace_bytes", "symcon_forward", "symcon_backward", "symcon_check_device_error",
+           "symcon_workspace_bytes", "symcon_forward", "symcon_backward", "symcon_backward_ex", "symcon_check_device_error",
            "symcon_last_launch_count", "symcon_destroy", "symcon_status_string", "symcon_last_error",
            "symcon_pack_balanced", "symcon_precompile", "symcon_plan_source", "symcon_profile_enable",
            "symcon_profile_reset", "symcon_profile_read"]
@@ -46,6 +46,8 @@ lib.symcon_workspace_bytes.argtypes = [_vp, _i64]
 lib.symcon_workspace_bytes.restype = _sz
 lib.symcon_forward.argtypes = [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
 lib.symcon_backward.argtypes = [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
+lib.symcon_backward_ex.argtypes = [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, ctypes.c_uint32, _vp]
+SYMCON_REUSE_BUCKETS, SYMCON_REUSE_FOLD = 1, 2
 lib.symcon_check_device_error.argtypes = [_vp, _vp, _vp, ctypes.POINTER(_i64)]
 lib.symcon_last_launch_count.argtypes = [_vp]
 lib.symcon_last_launch_count.restype = _i32
@@ -65,7 +67,7 @@ lib.symcon_profile_read.argtypes = [_vp, ctypes.POINTER(ctypes.c_char_p), ctypes
                                     ctypes.POINTER(ctypes.c_double)]
 lib.symcon_profile_read.restype = _i32
 for _n in ("symcon_profile_enable", "symcon_profile_reset", "symcon_build_tables", "symcon_plan_info", "symcon_plan_path", "symcon_plan_sym_table", "symcon_real_cg",
-           "symcon_forward", "symcon_backward", "symcon_check_device_error", "symcon_pack_balanced",
+           "symcon_forward", "symcon_backward", "symcon_backward_ex", "symcon_check_device_error", "symcon_pack_balanced",
            "symcon_precompile"):
     getattr(lib, _n).restype = ctypes.c_int
 
@@ -142,6 +144,11 @@ def symcon_forward(plan, num_nodes, A, W, node_elem, B, ws, ws_bytes, stream):
 
 def symcon_backward(plan, num_nodes, A, W, node_elem, dB, dA, dW, ws, ws_bytes, stream):
     check(lib.symcon_backward(plan, num_nodes, A, W, node_elem, dB, dA, dW, ws, ws_bytes, stream), "symcon_backward")
+
+
+def symcon_backward_ex(plan, num_nodes, A, W, node_elem, dB, dA, dW, ws, ws_bytes, flags, stream):
+    check(lib.symcon_backward_ex(plan, num_nodes, A, W, node_elem, dB, dA, dW, ws, ws_bytes, flags, stream),
+          "symcon_backward_ex")
 
 
 def symcon_check_device_error(plan, ws, stream):

@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <map>
 #include <mutex>
 #include <sstream>
 #include <string>
@@ -46,6 +47,10 @@ struct symcon_plan {
   mutable std::vector<cudaEvent_t> event_pool;
   mutable double prof_ms[8] = {0};
   mutable int64_t prof_n[8] = {0};
+  // per-workspace record of what the last call left in it (for the SYMCON_REUSE_* hints)
+  struct WsState { int64_t N = -1; const void* ne = nullptr; const void* W = nullptr; };
+  mutable std::mutex ws_mu;
+  mutable std::map<const void*, WsState> ws_state;
 };
 
 static const char* kKindNames[] = {"symcon_bucket", "symcon_fold", "symcon_fwd", "symcon_bwd_dA", "symcon_bwd_dW",
@@ -457,8 +462,20 @@ static void fill_params(const symcon_plan* p, const WsLayout& w, char* ws, int64
 }
 
 static int launch_prep(const symcon_plan* p, const WsLayout& w, char* ws, int64_t N, const int32_t* ne, const float* W,
-                       Params& q, cudaStream_t st, bool fold, symcon_status* s) {
+                       Params& q, cudaStream_t st, bool fold, symcon_status* s, uint32_t flags = 0) {
   int n = 0;
+  bool skip_bucket = false, skip_fold = false;
+  {
+    std::lock_guard<std::mutex> g(p->ws_mu);
+    auto& rec = p->ws_state[ws];
+    skip_bucket = (flags & SYMCON_REUSE_BUCKETS) && rec.N == N && rec.ne == ne;
+    skip_fold = (flags & SYMCON_REUSE_FOLD) && skip_bucket && rec.W == W;
+    rec.N = N;
+    rec.ne = ne;
+    if (fold) rec.W = W;
+  }
+  if (skip_fold) fold = false;
+  if (skip_bucket) goto after_bucket;
   BucketArgs b;
   b.node_elem = ne;
   b.N = (int)N;
@@ -482,6 +499,7 @@ static int launch_prep(const symcon_plan* p, const WsLayout& w, char* ws, int64_
     Timed tm(p, K_BUCKET, st);
     n += bucket_launch(b, st);
   }
+after_bucket:
   if (fold) {
     Timed tm(p, K_FOLD, st);
     q.W = W;
@@ -526,6 +544,12 @@ symcon_status symcon_forward(const symcon_plan* p, int64_t N, const float* A, co
 
 symcon_status symcon_backward(const symcon_plan* p, int64_t N, const float* A, const float* W, const int32_t* ne,
                               const float* dB, float* dA, float* dW, void* ws, size_t ws_bytes, void* stream) {
+  return symcon_backward_ex(p, N, A, W, ne, dB, dA, dW, ws, ws_bytes, 0u, stream);
+}
+
+symcon_status symcon_backward_ex(const symcon_plan* p, int64_t N, const float* A, const float* W, const int32_t* ne,
+                                 const float* dB, float* dA, float* dW, void* ws, size_t ws_bytes, uint32_t flags,
+                                 void* stream) {
   if (!p) { set_error("plan is NULL"); return SYMCON_EINVAL; }
   cudaStream_t st = (cudaStream_t)stream;
   p->last_launches = 0;
@@ -548,7 +572,7 @@ symcon_status symcon_backward(const symcon_plan* p, int64_t N, const float* A, c
   q.dB = dB;
   q.dA = dA;
   q.dW = dW;
-  int n = launch_prep(p, w, (char*)ws, N, ne, W, q, st, dA != nullptr, &s);
+  int n = launch_prep(p, w, (char*)ws, N, ne, W, q, st, dA != nullptr, &s, flags);
   if (s) return s;
   void* args[] = {&q};
   const unsigned ky = (p->t.K + p->kc.warps_per_cta - 1) / p->kc.warps_per_cta;

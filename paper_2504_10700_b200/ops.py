@@ -78,7 +78,10 @@ class SymmetricContraction:
                             ws.data_ptr(), ws.numel(), _stream_ptr(self.device))
         return B
 
-    def backward_raw(self, A, W, node_elem, dB, need_dA=True, need_dW=True, dA=None, dW=None, ws_key="default"):
+    def backward_raw(self, A, W, node_elem, dB, need_dA=True, need_dW=True, dA=None, dW=None, ws_key="default",
+                     reuse=False):
+        """reuse=True passes SYMCON_REUSE_BUCKETS|FOLD: the bucketing and W-fold left in the
+        workspace by the preceding forward (same node_elem / W tensors) are reused."""
         N = self._check(A, W, node_elem)
         assert dB.dtype == torch.float32 and dB.is_contiguous() and dB.shape == (N, self.out_dim)
         if need_dA and dA is None:
@@ -86,9 +89,10 @@ class SymmetricContraction:
         if need_dW and dW is None:
             dW = torch.empty_like(W)
         ws = self.workspace(N, ws_key)
-        _lib.symcon_backward(self.plan, N, A.data_ptr(), W.data_ptr(), node_elem.data_ptr(), dB.data_ptr(),
-                             dA.data_ptr() if need_dA else None, dW.data_ptr() if need_dW else None,
-                             ws.data_ptr(), ws.numel(), _stream_ptr(self.device))
+        flags = (_lib.SYMCON_REUSE_BUCKETS | _lib.SYMCON_REUSE_FOLD) if reuse else 0
+        _lib.symcon_backward_ex(self.plan, N, A.data_ptr(), W.data_ptr(), node_elem.data_ptr(), dB.data_ptr(),
+                                dA.data_ptr() if need_dA else None, dW.data_ptr() if need_dW else None,
+                                ws.data_ptr(), ws.numel(), flags, _stream_ptr(self.device))
         return (dA if need_dA else None), (dW if need_dW else None)
 
     def check_device_error(self, ws_key="default"):
@@ -115,5 +119,6 @@ class _SymconFn(torch.autograd.Function):
     @staticmethod
     def backward(ctx, dB):
         A, W, node_elem = ctx.saved_tensors
-        dA, dW = ctx.sc.backward_raw(A, W, node_elem, dB.contiguous(), ctx.needs_input_grad[0], ctx.needs_input_grad[1])
+        dA, dW = ctx.sc.backward_raw(A, W, node_elem, dB.contiguous(), ctx.needs_input_grad[0], ctx.needs_input_grad[1],
+                                     reuse=True)
         return dA, dW, None, None

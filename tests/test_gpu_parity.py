@@ -204,3 +204,20 @@ def test_autograd_wrapper():
     dA, dW = sc.backward_raw(A.detach(), W.detach(), ne, dB)
     torch.cuda.synchronize()
     assert torch.equal(A.grad, dA) and torch.equal(W.grad, dW)
+
+
+def test_reuse_hints_never_change_results():
+    sc = _sc(3, 3, (0, 1), 7, 32)
+    A, W, ne, dB = _inputs(sc, 900, "zipf")
+    ref_dA, ref_dW = sc.backward_raw(A, W, ne, dB)
+    sc.forward_raw(A, W, ne)
+    dA1, dW1 = sc.backward_raw(A, W, ne, dB, reuse=True)          # reuses buckets + fold
+    ne2 = ne.flip(0).contiguous()                                   # different pointer and contents
+    sc.forward_raw(A, W, ne2)
+    dA2, dW2 = sc.backward_raw(A, W, ne, dB, reuse=True)           # hint must not apply: redone
+    W2 = (W * 2).contiguous()
+    sc.forward_raw(A, W2, ne)
+    dA3, _ = sc.backward_raw(A, W, ne, dB, reuse=True)             # same ne, other W: fold redone
+    torch.cuda.synchronize()
+    for x, y in ((dA1, ref_dA), (dW1, ref_dW), (dA2, ref_dA), (dW2, ref_dW), (dA3, ref_dA)):
+        assert torch.equal(x, y)
