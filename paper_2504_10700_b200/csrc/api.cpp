@@ -33,7 +33,8 @@ struct symcon_plan {
   KernelConfig kc;
   int device = -1;
   int npad = 0;
-  size_t unfold_smem = 0, tile_smem = 0;
+  size_t unfold_smem = 0, tile_smem = 0, dw_smem = 0;
+  int dw_gpc = 1, dw_nz = 1;
   int grid_fwd = 0, grid_dA = 0;
   std::string source;
   cudaLibrary_t lib = nullptr;
@@ -105,10 +106,12 @@ struct Params {  // must match SymconParams in codegen.cpp
   int N, K, E, pad;
   float zero;
   const int* tile_perm;
+  float* stot;
 };
 
 struct WsLayout {
-  size_t hist, off, seg_off, perm, tiles, n_tiles, items, n_items, item_off, err, coef, spart, tile_off, tile_perm, total;
+  size_t hist, off, seg_off, perm, tiles, n_tiles, items, n_items, item_off, err, coef, spart, tile_off, tile_perm, stot,
+      total;
   int64_t max_tiles, max_items;
 };
 
@@ -136,6 +139,7 @@ WsLayout layout(const symcon_plan* p, int64_t N) {
   w.tile_perm = take(sizeof(int) * (size_t)w.max_tiles * p->kc.tile_nodes);
   w.coef = take(sizeof(float) * (size_t)E * K * p->npad);
   w.spart = take(sizeof(float) * (size_t)w.max_items * K * p->npad);
+  w.stot = take(sizeof(float) * (size_t)E * K * p->npad);
   w.total = o;
   return w;
 }
@@ -332,6 +336,15 @@ symcon_status symcon_build_tables(int lmax_in, int correlation, const int* out_L
       p->grid_fwd = sms * std::max(occ_f, 1);
       p->grid_dA = sms * std::max(occ_a, 1);
     }
+    {
+      const int nout = p->t.out_per_ch, nrows = (int)p->t.rows.size();
+      const int ng = (nrows + p->kc.dw_rows_per_group - 1) / p->kc.dw_rows_per_group;  // must match codegen
+      p->dw_gpc = std::min(ng, p->kc.dw_groups_per_cta);
+      p->dw_nz = (ng + p->dw_gpc - 1) / p->dw_gpc;
+      p->dw_smem = sizeof(float) * (size_t)p->kc.dw_block_nodes * (p->t.n_lm + nout) * 34;
+      if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_dW, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                           (int)p->dw_smem, device), "dW smem attribute");
+    }
     p->unfold_smem = sizeof(float) * 32 * (size_t)(p->npad + 1);
     if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_unfold, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                          (int)p->unfold_smem, device), "unfold smem attribute");
@@ -455,6 +468,7 @@ static void fill_params(const symcon_plan* p, const WsLayout& w, char* ws, int64
   q.coef = (float*)(ws + w.coef);
   q.spart = (float*)(ws + w.spart);
   q.tile_perm = (const int*)(ws + w.tile_perm);
+  q.stot = (float*)(ws + w.stot);
   q.N = (int)N;
   q.K = p->t.K;
   q.E = p->t.E;
@@ -579,11 +593,12 @@ symcon_status symcon_backward_ex(const symcon_plan* p, int64_t N, const float* A
   if (dW) {
     {
     Timed tm(p, K_DW, st);
-    s = cuda_err(cudaLaunchKernel((const void*)p->k_dW, dim3((unsigned)w.max_items, ky), dim3(32 * p->kc.warps_per_cta),
-                                  args, 0, st), "launch symcon_bwd_dW");
+    s = cuda_err(cudaLaunchKernel((const void*)p->k_dW, dim3((unsigned)w.max_items, (p->t.K + 31) / 32, p->dw_nz),
+                                  dim3(32 * p->dw_gpc), args, p->dw_smem, st), "launch symcon_bwd_dW");
     }
     if (s) return s;
     Timed tm(p, K_UNFOLD, st);
+    n += reduce_items_launch(q.spart, q.item_off, p->t.E, p->npad, p->t.K, q.stot, st);
     s = cuda_err(cudaLaunchKernel((const void*)p->k_unfold, dim3(p->t.E, (p->t.K + 31) / 32), dim3(512), args,
                                   p->unfold_smem, st), "launch symcon_unfold");
     if (s) return s;

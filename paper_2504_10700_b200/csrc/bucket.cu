@@ -158,6 +158,34 @@ int fill_nan_launch(const int* perm, const int* seg_off, int E, float* out, long
   return 1;
 }
 
+// Fixed-order segmented sum of the dW S partials over each element's items (the items of an
+// element are contiguous). One thread per (z, j, k); 4-way unrolled loads for memory parallelism,
+// summed in item order so the result is bitwise deterministic.
+__global__ void dw_reduce_items(const float* __restrict__ spart, const int* __restrict__ item_off, int npad, int K,
+                                float* __restrict__ stot) {
+  const int z = blockIdx.y;
+  const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long per = (long long)npad * K;
+  if (slot >= per) return;
+  const int it0 = item_off[z], it1 = item_off[z + 1];
+  float s = 0.f;
+  int it = it0;
+  for (; it + 4 <= it1; it += 4) {
+    const float a = spart[it * per + slot], b = spart[(it + 1) * per + slot];
+    const float c = spart[(it + 2) * per + slot], d = spart[(it + 3) * per + slot];
+    s += a; s += b; s += c; s += d;
+  }
+  for (; it < it1; it++) s += spart[it * per + slot];
+  stot[(long long)z * per + slot] = s;
+}
+
+int reduce_items_launch(const float* spart, const int* item_off, int E, int npad, int K, float* stot, cudaStream_t st) {
+  const long long per = (long long)npad * K;
+  dim3 grid((unsigned)((per + 255) / 256), E);
+  dw_reduce_items<<<grid, 256, 0, st>>>(spart, item_off, npad, K, stot);
+  return 1;
+}
+
 size_t bucket_chunks(int64_t N) { return (size_t)((N + kChunk - 1) / kChunk); }
 
 }  // namespace symcon

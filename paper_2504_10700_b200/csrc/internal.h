@@ -48,9 +48,12 @@ struct KernelConfig {
   int warps_per_cta = 8;     // dW kernel: channels per CTA (one warp per channel)
   int tile_warps = 4;        // fwd / dA persistent kernels: warps (channels) per CTA
   int tile_nodes = 64;       // nodes per tile: 2 per lane
-  int dw_tiles_per_item = 8; // tiles per dW work item
+  int dw_tiles_per_item = 4; // tiles per dW work item
   int dw_tiles_per_butterfly = 2;  // tiles whose products are summed before one cross-lane reduction
   int dw_min_blocks = 2;           // __launch_bounds__ min blocks of the dW kernel
+  int dw_rows_per_group = 26;      // transposed dW: rows j per warp (register accumulators)
+  int dw_groups_per_cta = 16;      // transposed dW: warps per CTA
+  int dw_block_nodes = 8;          // transposed dW: nodes per smem stage
   int unfold_channels = 8;   // channels per unfold CTA
 };
 std::string generate_source(const Tables& t, const KernelConfig& kc);
