@@ -55,6 +55,8 @@ class OracleC:
                          *[self._arr[n].ctypes.data for n in ("col", "nu", "tup", "blk", "wid", "mpos", "u")])
         self.n_terms = len(rows)
         self.lib.oracle_num_threads.restype = ctypes.c_int
+        # use every core of this process's affinity mask (torchrun exports OMP_NUM_THREADS=1)
+        self.lib.oracle_set_threads(ctypes.c_int(len(os.sched_getaffinity(0))))
 
     def threads(self):
         return self.lib.oracle_num_threads()

@@ -1,0 +1,87 @@
+"""Data-parallel sharding of the contraction over bin-packed molecular graphs.
+
+* BinPackedShards: Alg. 1 (C++ partitioner in libsymcon) over the epoch's
+  graph sizes with capacity C and G = world size; bin j runs on rank j % G at step j // G
+  (reading s18). Every rank computes the same plan (deterministic, stable sorts,
+  PAPER.md:477), so no plan broadcast is needed.
+* DataParallelContraction: one training step of the contraction on this rank's bin: forward,
+  backward dW, NCCL all-reduce of dW (the one cross-GPU exchange; PAPER.md:960 DDP all-reduce)
+  on a communication stream, overlapped with the backward dA kernel.
+"""
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+
+
+class BinPackedShards:
+    def __init__(self, sizes, capacity, world, rank):
+        self.sizes = np.ascontiguousarray(sizes, dtype=np.int64)
+        self.capacity, self.world, self.rank = int(capacity), int(world), int(rank)
+        self.offsets, self.ids = _lib.symcon_pack_balanced(self.sizes, self.capacity, self.world)
+        self.n_bins = len(self.offsets) - 1
+        assert self.n_bins % self.world == 0
+        self.n_steps = self.n_bins // self.world
+
+    def bin_of(self, step, rank=None):
+        return step * self.world + (self.rank if rank is None else rank)
+
+    def graphs(self, step, rank=None):
+        b = self.bin_of(step, rank)
+        return self.ids[self.offsets[b]:self.offsets[b + 1]]
+
+    def nodes(self, step, rank=None):
+        return int(self.sizes[self.graphs(step, rank)].sum())
+
+    def step_imbalance(self, step):
+        """max / mean nodes over ranks at one step (1.0 = perfect balance)."""
+        loads = np.array([self.nodes(step, r) for r in range(self.world)], dtype=np.float64)
+        return float(loads.max() / max(loads.mean(), 1.0))
+
+    def bin_loads(self):
+        return np.add.reduceat(self.sizes[self.ids], self.offsets[:-1]) if self.n_bins else np.zeros(0)
+
+
+class DataParallelContraction:
+    """Forward + backward of one rank's bin with the dW all-reduce overlapped with dA."""
+
+    def __init__(self, sc, group=None, overlap=True):
+        self.sc = sc
+        self.group = group
+        self.overlap = overlap
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.comm = torch.cuda.Stream(device=sc.device) if self.world > 1 else None
+        self.launches = 0
+
+    def forward(self, A, W, node_elem, B=None):
+        B = self.sc.forward_raw(A, W, node_elem, B=B)
+        self.launches += self.sc.last_launch_count()
+        return B
+
+    def backward(self, A, W, node_elem, dB, dA=None, dW=None):
+        sc = self.sc
+        if self.world == 1:
+            dA, dW = sc.backward_raw(A, W, node_elem, dB, dA=dA, dW=dW, reuse=True)
+            self.launches += sc.last_launch_count()
+            return dA, dW
+        main = torch.cuda.current_stream(sc.device)
+        if not self.overlap:
+            dA, dW = sc.backward_raw(A, W, node_elem, dB, dA=dA, dW=dW, reuse=True)
+            self.launches += sc.last_launch_count()
+            dist.all_reduce(dW, group=self.group)
+            return dA, dW
+        # dW first (bucketing and W-fold reused from the forward), then all-reduce on the comm
+        # stream while the dA kernel runs on the main stream
+        _, dW = sc.backward_raw(A, W, node_elem, dB, need_dA=False, dW=dW, reuse=True)
+        self.launches += sc.last_launch_count()
+        ev = torch.cuda.Event()
+        ev.record(main)
+        self.comm.wait_event(ev)
+        with torch.cuda.stream(self.comm):
+            dist.all_reduce(dW, group=self.group)
+        dW.record_stream(self.comm)
+        dA, _ = sc.backward_raw(A, W, node_elem, dB, need_dW=False, dA=dA, reuse=True)
+        self.launches += sc.last_launch_count()
+        main.wait_stream(self.comm)
+        return dA, dW
