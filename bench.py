@@ -88,51 +88,52 @@ def alg_ops(sc):
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = "index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
-             "clocks_event_reasons.sw_power_cap"
+    """SM clock and throttle reasons sampled DURING the timed region (NVML, every 2 ms; falls
+    back to nvidia-smi -lms 100 if NVML is unavailable)."""
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4,
+               "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, index):
         self.index = index
-        self.p = None
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        import pynvml
+        h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+            r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+            for name, bit in self.REASONS.items():
+                if r & bit:
+                    self.reasons.add(name)
+            time.sleep(0.002)
 
     def __enter__(self):
         try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
-                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self.p = None
+            import pynvml
+            pynvml.nvmlInit()
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        except Exception:  # noqa: BLE001
+            self._t = None
         return self
 
     def __exit__(self, *a):
-        self.out = ""
-        if self.p:
-            time.sleep(0.25)
-            self.p.terminate()
-            try:
-                self.out, _ = self.p.communicate(timeout=5)
-            except Exception:
-                self.p.kill()
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in (self.out or "").strip().splitlines():
-            f = [x.strip() for x in line.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
-            except ValueError:
-                continue
-            for n, v in zip(names, f[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
+        sm = self.samples
+        mx = self.max_mhz
         load = [s for s in sm if mx and s > 0.5 * mx] or sm
-        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_min_mhz": min(load) if load else None,
+                "sm_max_mhz": mx, "reasons": sorted(self.reasons), "samples": len(sm), "source": "nvml 2ms"}
 
 
 # ----------------------------------------------------------------------------- cpu oracle

@@ -110,7 +110,7 @@ struct Params {  // must match SymconParams in codegen.cpp
 };
 
 struct WsLayout {
-  size_t hist, off, seg_off, perm, tiles, n_tiles, items, n_items, item_off, err, coef, spart, tile_off, tile_perm, stot,
+  size_t hist, chunk_bad, off, seg_off, perm, tiles, n_tiles, items, n_items, item_off, err, coef, spart, tile_off, tile_perm, stot,
       total;
   int64_t max_tiles, max_items;
 };
@@ -127,6 +127,7 @@ WsLayout layout(const symcon_plan* p, int64_t N) {
   auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes); return r; };
   w.err = take(sizeof(unsigned long long));  // first: its offset must not depend on N
   w.hist = take(sizeof(int) * nch * (E + 1));
+  w.chunk_bad = take(sizeof(int) * std::max<size_t>(nch, 1));
   w.off = take(sizeof(int) * nch * (E + 1));
   w.seg_off = take(sizeof(int) * (E + 2));
   w.perm = take(sizeof(int) * std::max<int64_t>(N, 1));
@@ -281,6 +282,11 @@ static symcon_status build_common(int lmax_in, int corr, const int* out_L, int n
   if (s) return s;
   auto* p = new (std::nothrow) symcon_plan();
   if (!p) return SYMCON_ENOMEM;
+  if (!parse_kernel_config(getenv("SYMCON_KCONFIG"), p->kc)) {
+    set_error("bad SYMCON_KCONFIG");
+    delete p;
+    return SYMCON_EINVAL;
+  }
   std::vector<int> ol(out_L, out_L + n_out);
   if (!build_tables(lmax_in, corr, ol, E, K, p->t)) { delete p; return SYMCON_EINVAL; }
   p->npad = (int)((p->t.rows.size() + 31) / 32 * 32);
@@ -321,7 +327,7 @@ symcon_status symcon_build_tables(int lmax_in, int correlation, const int* out_L
     if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_dA, p->lib, "symcon_bwd_dA"), "get symcon_bwd_dA");
     if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_dW, p->lib, "symcon_bwd_dW"), "get symcon_bwd_dW");
     if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_unfold, p->lib, "symcon_unfold"), "get symcon_unfold");
-    p->tile_smem = sizeof(float) * (size_t)p->kc.tile_warps * (2 * (size_t)p->npad);
+    p->tile_smem = sizeof(float) * (size_t)p->kc.tile_warps * (2 * (size_t)p->npad) + 16 * (size_t)p->kc.tile_warps;
     if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                          (int)p->tile_smem, device), "fwd smem attribute");
     if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_dA, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -509,6 +515,7 @@ static int launch_prep(const symcon_plan* p, const WsLayout& w, char* ws, int64_
   b.tile_off = (int*)(ws + w.tile_off);
   b.tile_perm = (int*)(ws + w.tile_perm);
   b.max_tiles = w.max_tiles;
+  b.chunk_bad = (int*)(ws + w.chunk_bad);
   {
     Timed tm(p, K_BUCKET, st);
     n += bucket_launch(b, st);
@@ -519,7 +526,7 @@ after_bucket:
     q.W = W;
     void* args[] = {&q};
     dim3 grid(p->t.E, (p->t.K + 31) / 32);
-    *s = cuda_err(cudaLaunchKernel((const void*)p->k_fold, grid, dim3(32), args, 0, st), "launch symcon_fold");
+    *s = cuda_err(cudaLaunchKernel((const void*)p->k_fold, grid, dim3(128), args, 0, st), "launch symcon_fold");
     n++;
   }
   return n;
@@ -550,8 +557,6 @@ symcon_status symcon_forward(const symcon_plan* p, int64_t N, const float* A, co
   }
   n++;
   if (s) return s;
-  Timed tn(p, K_NAN, st);
-  n += fill_nan_launch(q.perm, q.seg_off, p->t.E, B, (long long)p->t.K * p->t.out_per_ch, st);
   p->last_launches = n;
   return cuda_err(cudaGetLastError(), "forward launch");
 }
@@ -612,8 +617,6 @@ symcon_status symcon_backward_ex(const symcon_plan* p, int64_t N, const float* A
     }
     if (s) return s;
     n++;
-    Timed tn(p, K_NAN, st);
-    n += fill_nan_launch(q.perm, q.seg_off, p->t.E, dA, (long long)p->t.K * p->t.n_lm, st);
   }
   p->last_launches = n;
   return cuda_err(cudaGetLastError(), "backward launch");

@@ -19,9 +19,11 @@ namespace symcon {
 static constexpr int kChunk = 1024;
 
 __global__ void bk_hist(const int* __restrict__ ne, int N, int E, int* __restrict__ hist,
-                        unsigned long long* err) {
+                        int* __restrict__ chunk_bad) {
   extern __shared__ int h[];
+  __shared__ int bad;
   for (int e = threadIdx.x; e <= E; e += blockDim.x) h[e] = 0;
+  if (threadIdx.x == 0) bad = 0x7fffffff;
   __syncthreads();
   const int base = blockIdx.x * kChunk;
   for (int t = threadIdx.x; t < kChunk; t += blockDim.x) {
@@ -30,26 +32,34 @@ __global__ void bk_hist(const int* __restrict__ ne, int N, int E, int* __restric
     int e = ne[i];
     if (e < 0 || e >= E) {
       e = E;
-      atomicMin(err, (unsigned long long)i);
+      atomicMin(&bad, i);
     }
     atomicAdd(&h[e], 1);
   }
   __syncthreads();
   for (int e = threadIdx.x; e <= E; e += blockDim.x) hist[(size_t)blockIdx.x * (E + 1) + e] = h[e];
+  if (threadIdx.x == 0) chunk_bad[blockIdx.x] = bad;
 }
 
 __global__ void bk_scan(const int* __restrict__ hist, int nchunks, int E, int* __restrict__ off,
                         int* __restrict__ seg_off, int4* __restrict__ tiles, int* __restrict__ n_tiles,
                         int4* __restrict__ items, int* __restrict__ n_items, int* __restrict__ item_off,
-                        int* __restrict__ tile_off, int tile_nodes, int tiles_per_item) {
+                        int* __restrict__ tile_off, int* __restrict__ tile_perm, int tile_nodes, int tiles_per_item,
+                        const int* __restrict__ chunk_bad, unsigned long long* __restrict__ err) {
   extern __shared__ int sm[];   // tot[E+1], tile_off[E+1], itm_off[E+1]
   int* tot = sm;
   int* toff = sm + (E + 1);
   int* ioff = sm + 2 * (E + 1);
   for (int e = threadIdx.x; e <= E; e += blockDim.x) {
     int s = 0;
+#pragma unroll 8
     for (int c = 0; c < nchunks; c++) s += hist[(size_t)c * (E + 1) + e];
     tot[e] = s;
+  }
+  if (threadIdx.x == 0) {
+    int b = 0x7fffffff;
+    for (int c = 0; c < nchunks; c++) b = min(b, chunk_bad[c]);
+    *err = (b == 0x7fffffff) ? ~0ull : (unsigned long long)b;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -77,6 +87,7 @@ __global__ void bk_scan(const int* __restrict__ hist, int nchunks, int E, int* _
   __syncthreads();
   for (int e = threadIdx.x; e <= E; e += blockDim.x) {
     int r = tot[e];
+#pragma unroll 8
     for (int c = 0; c < nchunks; c++) {
       off[(size_t)c * (E + 1) + e] = r;
       r += hist[(size_t)c * (E + 1) + e];
@@ -89,6 +100,8 @@ __global__ void bk_scan(const int* __restrict__ hist, int nchunks, int E, int* _
         int c = min(tile_nodes, cnt - c0);
         tiles[toff[e] + t] = make_int4(e, start + c0, c, t);
       }
+      if (nt > 0)  // empty slots of the element's last tile (the scatter fills the others)
+        for (int q = cnt - (nt - 1) * tile_nodes; q < tile_nodes; q++) tile_perm[(size_t)(toff[e] + nt - 1) * tile_nodes + q] = -1;
       const int ni = (nt + tiles_per_item - 1) / tiles_per_item;
       for (int q = 0; q < ni; q++) {
         int t0 = q * tiles_per_item;
@@ -106,13 +119,21 @@ __global__ void bk_scatter(const int* __restrict__ ne, int N, int E, const int* 
   for (int e = lane; e <= E; e += 32) cnt[e] = off[(size_t)blockIdx.x * (E + 1) + e];
   __syncwarp();
   const int base = blockIdx.x * kChunk;
-  for (int g = 0; g < kChunk; g += 32) {
-    const int i = base + g + lane;
+  int ev[kChunk / 32];  // all 32 groups' elements in flight at once (latency hiding)
+#pragma unroll
+  for (int g = 0; g < kChunk / 32; g++) {
+    const int i = base + g * 32 + lane;
     int e = -1;
     if (i < N) {
       e = ne[i];
       if (e < 0 || e >= E) e = E;
     }
+    ev[g] = e;
+  }
+#pragma unroll
+  for (int g = 0; g < kChunk / 32; g++) {
+    const int i = base + g * 32 + lane;
+    const int e = ev[g];
     const unsigned peers = __match_any_sync(0xffffffffu, e);
     const int rank = __popc(peers & ((1u << lane) - 1u));
     const int leader = __ffs(peers) - 1;
@@ -142,11 +163,10 @@ __global__ void bk_fill_nan(const int* __restrict__ perm, const int* __restrict_
 int bucket_launch(const BucketArgs& a, cudaStream_t st) {
   const int nchunks = (a.N + kChunk - 1) / kChunk;
   const size_t sm_e = sizeof(int) * (a.E + 1);
-  cudaMemsetAsync(a.err, 0xff, sizeof(unsigned long long), st);
-  if (a.N > 0) bk_hist<<<nchunks, 256, sm_e, st>>>(a.node_elem, a.N, a.E, a.hist, a.err);
+  if (a.N > 0) bk_hist<<<nchunks, 256, sm_e, st>>>(a.node_elem, a.N, a.E, a.hist, a.chunk_bad);
   bk_scan<<<1, 256, 3 * sm_e, st>>>(a.hist, nchunks, a.E, a.off, a.seg_off, a.tiles, a.n_tiles, a.items,
-                                    a.n_items, a.item_off, a.tile_off, a.tile_nodes, a.tiles_per_item);
-  cudaMemsetAsync(a.tile_perm, 0xff, sizeof(int) * (size_t)a.max_tiles * a.tile_nodes, st);
+                                    a.n_items, a.item_off, a.tile_off, a.tile_perm, a.tile_nodes, a.tiles_per_item,
+                                    a.chunk_bad, a.err);
   if (a.N > 0)
     bk_scatter<<<nchunks, 32, sm_e, st>>>(a.node_elem, a.N, a.E, a.off, a.seg_off, a.tile_off, a.tile_nodes, a.perm,
                                           a.tile_perm);

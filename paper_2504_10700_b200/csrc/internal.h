@@ -46,7 +46,11 @@ bool build_tables(int lmax_in, int corr, const std::vector<int>& out_L, int E, i
 // ---- codegen.cpp
 struct KernelConfig {
   int warps_per_cta = 8;     // dW kernel: channels per CTA (one warp per channel)
-  int tile_warps = 4;        // fwd / dA persistent kernels: warps (channels) per CTA
+  int tile_warps = 2;        // fwd / dA persistent kernels: warps (channels) per CTA
+  bool coef_tma = false;     // stage coefficients with cp.async.bulk + mbarrier (else per-lane cp.async)
+  int tile_min_blocks = 1;   // __launch_bounds__ min blocks for fwd / dA (caps registers)
+  int coef_lookahead = 3;    // coefficient quads loaded ahead of first use
+  bool coef_unroll = false;  // unroll the per-lane cp.async loop of the coefficient staging
   int tile_nodes = 64;       // nodes per tile: 2 per lane
   int dw_tiles_per_item = 4; // tiles per dW work item
   int dw_tiles_per_butterfly = 2;  // tiles whose products are summed before one cross-lane reduction
@@ -57,6 +61,8 @@ struct KernelConfig {
   int unfold_channels = 8;   // channels per unfold CTA
 };
 std::string generate_source(const Tables& t, const KernelConfig& kc);
+// apply "key=value,..." overrides (env SYMCON_KCONFIG) to a KernelConfig; returns false on bad keys
+bool parse_kernel_config(const char* spec, KernelConfig& kc);
 
 // ---- pack.cpp
 int64_t pack_balanced(const int64_t* sizes, int64_t n, int64_t C, int G,

@@ -20,6 +20,7 @@ struct BucketArgs {
   int* tile_off;  // [E+1]
   int* tile_perm; // [max_tiles][tile_nodes], -1 padded
   int64_t max_tiles;
+  int* chunk_bad;  // [nchunks] first out-of-range node of each chunk
   unsigned long long* err;
 };
 
