@@ -282,11 +282,15 @@ static symcon_status build_common(int lmax_in, int corr, const int* out_L, int n
   if (s) return s;
   auto* p = new (std::nothrow) symcon_plan();
   if (!p) return SYMCON_ENOMEM;
-  if (!parse_kernel_config(getenv("SYMCON_KCONFIG"), p->kc)) {
+  if (!parse_kernel_config(getenv("SYMCON_KCONFIG"), p->kc) || p->kc.node_pairs_per_lane < 1 ||
+      p->kc.node_pairs_per_lane > 2) {
     set_error("bad SYMCON_KCONFIG");
     delete p;
     return SYMCON_EINVAL;
   }
+  p->kc.tile_nodes = 64 * p->kc.node_pairs_per_lane;
+  // dW items: ~256 nodes
+  if (p->kc.node_pairs_per_lane == 2 && p->kc.dw_tiles_per_item == 4) p->kc.dw_tiles_per_item = 2;
   std::vector<int> ol(out_L, out_L + n_out);
   if (!build_tables(lmax_in, corr, ol, E, K, p->t)) { delete p; return SYMCON_EINVAL; }
   p->npad = (int)((p->t.rows.size() + 31) / 32 * 32);

@@ -53,7 +53,9 @@ struct KernelConfig {
   int coef_mode = 0;         // coefficient staging: 0 per-lane cp.async, 2 registers (LDG.128) + STS
   bool coef_volatile = true; // issue coefficient LDS with volatile asm at the lookahead position
   bool coef_unroll = false;  // unroll the per-lane cp.async loop of the coefficient staging
-  int tile_nodes = 64;       // nodes per tile: 2 per lane
+  int tile_nodes = 64;       // nodes per tile (= 64 * node_pairs_per_lane; set by the plan)
+  int node_pairs_per_lane = 1;  // fwd / dA: node pairs per lane (1 or 2)
+  bool a_prefetch = true;    // fwd / dA: prefetch the next item's A / dB rows into registers
   int dw_tiles_per_item = 4; // tiles per dW work item
   int dw_tiles_per_butterfly = 2;  // tiles whose products are summed before one cross-lane reduction
   int dw_min_blocks = 2;           // __launch_bounds__ min blocks of the dW kernel
