@@ -221,3 +221,76 @@ def test_reuse_hints_never_change_results():
     torch.cuda.synchronize()
     for x, y in ((dA1, ref_dA), (dW1, ref_dW), (dA2, ref_dA), (dW2, ref_dW), (dA3, ref_dA)):
         assert torch.equal(x, y)
+
+
+def test_full_size_off_small_all_nodes():
+    """OFF-small at full size (20k nodes of 10-100-atom molecules, 96 channels, 0e): every output
+    element against the C oracle."""
+    from oracle.contraction import Problem
+    from oracle.ceval import OracleC
+    from synth.inputs import CONFIGS, make_config_inputs
+    cfg = CONFIGS["off_small"]
+    sc = _sc(3, 3, cfg.out_L, cfg.n_elements, cfg.channels)
+    A, W, ne, dB = make_config_inputs(cfg, sc.block_sizes(), sc.out_dim, device="cuda")
+    B, dA, dW = _run(sc, A, W, ne, dB)
+    oc = OracleC(Problem(3, 3, cfg.out_L))
+    hA, hW, hne, hdB = _host(A, W, ne, dB)
+    assert _rel(B.cpu(), oc.forward(hA, hW, hne)) < TOL
+    dAref, dWref = oc.backward(hA, hW, hne, hdB)
+    assert _rel(dA.cpu(), dAref) < TOL
+    assert _rel(dW.cpu(), dWref) < TOL
+
+
+def test_full_size_large_sampled():
+    """Large (200k nodes, 256 channels, 0e+1o+2e): sampled nodes for B and dA, dW exactly on the
+    two smallest elements."""
+    from oracle.contraction import Problem
+    from oracle.ceval import OracleC
+    from synth.inputs import CONFIGS, make_config_inputs
+    cfg = CONFIGS["large"]
+    sc = _sc(3, 3, cfg.out_L, cfg.n_elements, cfg.channels)
+    A, W, ne, dB = make_config_inputs(cfg, sc.block_sizes(), sc.out_dim, device="cuda")
+    B, dA, dW = _run(sc, A, W, ne, dB)
+    oc = OracleC(Problem(3, 3, cfg.out_L))
+    rng = np.random.default_rng(7)
+    idx = torch.tensor(np.sort(rng.choice(cfg.n_nodes, 48, replace=False)), device="cuda")
+    hA, hW, hne, hdB = _host(A[idx], W, ne[idx], dB[idx])
+    assert _rel(B[idx].cpu(), oc.forward(hA, hW, hne)) < TOL
+    dAref, _ = oc.backward(hA, hW, hne, hdB, want_dW=False)
+    assert _rel(dA[idx].cpu(), dAref) < TOL
+    counts = torch.bincount(ne.long(), minlength=cfg.n_elements).cpu().numpy()
+    for z in np.argsort(counts)[:2]:
+        sel = torch.nonzero(ne == int(z)).flatten()
+        hA, hne, hdB = _host(A[sel], ne[sel], dB[sel])
+        _, dWref = oc.backward(hA, hW, hne, hdB, want_dA=False)
+        assert _rel(dW[z].cpu(), dWref[z]) < TOL
+    del A, dB, B, dA
+    torch.cuda.empty_cache()
+
+
+def test_sharded_dp_step_matches_single_pass():
+    """Data-parallel plumbing on one GPU: the dW of two bins computed separately and summed equals
+    the dW of their union (what the NCCL all-reduce produces across ranks), bitwise up to the
+    fp32 sum order tolerance."""
+    from synth.inputs import table2_sizes, graph_elements
+    from paper_2504_10700_b200.dist import BinPackedShards
+    sc = _sc(3, 3, (0, 1), 89, 64)
+    sizes = table2_sizes(scale=0.002)
+    sh = BinPackedShards(sizes, 3072, 2, 0)
+    parts = []
+    for r in range(2):
+        g = sh.graphs(0, r)
+        ne = torch.from_numpy(graph_elements(sizes[g], salt=r)).cuda()
+        A = torch.randn((ne.numel(), 64, 16), device="cuda")
+        dB = torch.randn((ne.numel(), sc.out_dim), device="cuda")
+        parts.append((A, ne, dB))
+    from synth.inputs import gen_W
+    W = gen_W(89, sc.block_sizes(), 64, "cuda")
+    dWs = [sc.backward_raw(A, W, ne, dB, need_dA=False)[1].clone() for A, ne, dB in parts]
+    Au = torch.cat([p[0] for p in parts]).contiguous()
+    neu = torch.cat([p[1] for p in parts]).contiguous()
+    dBu = torch.cat([p[2] for p in parts]).contiguous()
+    _, dWu = sc.backward_raw(Au, W, neu, dBu, need_dA=False)
+    torch.cuda.synchronize()
+    s = dWs[0] + dWs[1]
+    assert (s - dWu).abs().max().item() <= 1e-5 * dWu.abs().max().item()
