@@ -88,29 +88,32 @@ def alg_ops(sc):
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """SM clock and throttle reasons sampled DURING the timed region (NVML, every 2 ms; falls
-    back to nvidia-smi -lms 100 if NVML is unavailable)."""
+    """SM clock and throttle reasons sampled DURING the timed region: an NVML thread polls every
+    ~2 ms from before the region starts; samples are kept if they fall inside [start, end]
+    (marked by the caller) widened by 20 ms."""
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4,
                "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, index):
         self.index = index
-        self.samples = []
-        self.reasons = set()
+        self.samples = []          # (t, mhz, reasons)
         self.max_mhz = None
         self._stop = threading.Event()
+        self._ready = threading.Event()
         self._t = None
+        self.t0 = self.t1 = None
 
     def _run(self):
         import pynvml
-        h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-        self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        try:
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        finally:
+            self._ready.set()
         while not self._stop.is_set():
-            self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+            mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
             r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-            for name, bit in self.REASONS.items():
-                if r & bit:
-                    self.reasons.add(name)
+            self.samples.append((time.perf_counter(), mhz, r))
             time.sleep(0.002)
 
     def __enter__(self):
@@ -119,21 +122,33 @@ class ClockSampler:
             pynvml.nvmlInit()
             self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
+            self._ready.wait(timeout=5)
+            time.sleep(0.01)
         except Exception:  # noqa: BLE001
             self._t = None
         return self
 
+    def start(self):
+        self.t0 = time.perf_counter()
+
+    def end(self):
+        self.t1 = time.perf_counter()
+
     def __exit__(self, *a):
+        time.sleep(0.01)
         self._stop.set()
         if self._t:
             self._t.join(timeout=2)
 
     def summary(self):
-        sm = self.samples
+        t0 = (self.t0 or 0) - 0.02
+        t1 = (self.t1 or time.perf_counter()) + 0.02
+        win = [(m, r) for (t, m, r) in self.samples if t0 <= t <= t1]
         mx = self.max_mhz
-        load = [s for s in sm if mx and s > 0.5 * mx] or sm
-        return {"sm_mhz": statistics.median(load) if load else None, "sm_min_mhz": min(load) if load else None,
-                "sm_max_mhz": mx, "reasons": sorted(self.reasons), "samples": len(sm), "source": "nvml 2ms"}
+        sm = [m for m, _ in win]
+        reasons = sorted({name for _, r in win for name, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_min_mhz": min(sm) if sm else None,
+                "sm_max_mhz": mx, "reasons": reasons, "samples": len(sm), "source": "nvml ~2ms"}
 
 
 # ----------------------------------------------------------------------------- cpu oracle
@@ -265,11 +280,13 @@ def run_ours(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     nodes = 0
     with ClockSampler(local) as clk:
+        clk.start()
         e0.record()
         for q in range(args.steps):
             nodes += step(q)
         e1.record()
         torch.cuda.synchronize()
+        clk.end()
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)

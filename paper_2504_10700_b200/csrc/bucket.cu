@@ -41,7 +41,7 @@ __global__ void bk_hist(const int* __restrict__ ne, int N, int E, int* __restric
   if (threadIdx.x == 0) chunk_bad[blockIdx.x] = bad;
 }
 
-__global__ void bk_scan(const int* __restrict__ hist, int nchunks, int E, int* __restrict__ off,
+__global__ void __launch_bounds__(1024) bk_scan(const int* __restrict__ hist, int nchunks, int E, int* __restrict__ off,
                         int* __restrict__ seg_off, int4* __restrict__ tiles, int* __restrict__ n_tiles,
                         int4* __restrict__ items, int* __restrict__ n_items, int* __restrict__ item_off,
                         int* __restrict__ tile_off, int* __restrict__ tile_perm, int tile_nodes, int tiles_per_item,
@@ -50,19 +50,22 @@ __global__ void bk_scan(const int* __restrict__ hist, int nchunks, int E, int* _
   int* tot = sm;
   int* toff = sm + (E + 1);
   int* ioff = sm + 2 * (E + 1);
-  for (int e = threadIdx.x; e <= E; e += blockDim.x) {
-    int s = 0;
-#pragma unroll 8
-    for (int c = 0; c < nchunks; c++) s += hist[(size_t)c * (E + 1) + e];
-    tot[e] = s;
-  }
-  if (threadIdx.x == 0) {
-    int b = 0x7fffffff;
-    for (int c = 0; c < nchunks; c++) b = min(b, chunk_bad[c]);
-    *err = (b == 0x7fffffff) ? ~0ull : (unsigned long long)b;
-  }
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5, E1 = E + 1;
+  for (int e = tid; e <= E; e += blockDim.x) tot[e] = 0;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  // 1. element totals: coalesced pass over the [chunk][E+1] histogram with smem atomics
+  for (int x = tid; x < nchunks * E1; x += blockDim.x) {
+    const int h = hist[x];
+    if (h) atomicAdd(&tot[x % E1], h);
+  }
+  __shared__ int bad;
+  if (tid == 0) bad = 0x7fffffff;
+  __syncthreads();
+  for (int c = tid; c < nchunks; c += blockDim.x) atomicMin(&bad, chunk_bad[c]);
+  __syncthreads();
+  if (tid == 0) *err = (bad == 0x7fffffff) ? ~0ull : (unsigned long long)bad;
+  // 2. segment / tile / item offsets (serial over elements, tiny)
+  if (tid == 0) {
     int s = 0, ts = 0, is = 0;
     for (int e = 0; e <= E; e++) {
       int c = tot[e];
@@ -85,28 +88,36 @@ __global__ void bk_scan(const int* __restrict__ hist, int nchunks, int E, int* _
     item_off[E + 1] = is;
   }
   __syncthreads();
-  for (int e = threadIdx.x; e <= E; e += blockDim.x) {
-    int r = tot[e];
-#pragma unroll 8
-    for (int c = 0; c < nchunks; c++) {
-      off[(size_t)c * (E + 1) + e] = r;
-      r += hist[(size_t)c * (E + 1) + e];
+  // 3. per element (one warp each): exclusive scan over chunks -> off[c][e]; tiles, items, padding
+  for (int e = warp; e <= E; e += nw) {
+    int run = tot[e];
+    for (int c0 = 0; c0 < nchunks; c0 += 32) {
+      const int c = c0 + lane;
+      const int h = (c < nchunks) ? hist[(size_t)c * E1 + e] : 0;
+      int x = h;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (c < nchunks) off[(size_t)c * E1 + e] = run + x - h;
+      run += __shfl_sync(0xffffffffu, x, 31);
     }
     if (e < E) {
-      const int start = tot[e], cnt = r - tot[e];
+      const int start = tot[e], cnt = run - tot[e];
       const int nt = (cnt + tile_nodes - 1) / tile_nodes;
-      for (int t = 0; t < nt; t++) {
-        int c0 = t * tile_nodes;
-        int c = min(tile_nodes, cnt - c0);
-        tiles[toff[e] + t] = make_int4(e, start + c0, c, t);
+      for (int t = lane; t < nt; t += 32) {
+        const int c0 = t * tile_nodes;
+        tiles[toff[e] + t] = make_int4(e, start + c0, min(tile_nodes, cnt - c0), t);
       }
-      if (nt > 0)  // empty slots of the element's last tile (the scatter fills the others)
-        for (int q = cnt - (nt - 1) * tile_nodes; q < tile_nodes; q++) tile_perm[(size_t)(toff[e] + nt - 1) * tile_nodes + q] = -1;
       const int ni = (nt + tiles_per_item - 1) / tiles_per_item;
-      for (int q = 0; q < ni; q++) {
-        int t0 = q * tiles_per_item;
+      for (int q = lane; q < ni; q += 32) {
+        const int t0 = q * tiles_per_item;
         items[ioff[e] + q] = make_int4(e, toff[e] + t0, min(tiles_per_item, nt - t0), q);
       }
+      if (nt > 0)  // empty slots of the element's last tile (the scatter fills the others)
+        for (int q = cnt - (nt - 1) * tile_nodes + lane; q < tile_nodes; q += 32)
+          tile_perm[(size_t)(toff[e] + nt - 1) * tile_nodes + q] = -1;
     }
   }
 }
@@ -150,6 +161,48 @@ __global__ void bk_scatter(const int* __restrict__ ne, int N, int E, const int* 
   }
 }
 
+// Block-parallel stable scatter for E + 1 <= kWarpE: one CTA (32 warps) per 1024-node chunk.
+// Warp w ranks its 32 nodes with one __match_any_sync; per-warp element counts go to smem,
+// an exclusive scan over warps (per element) gives each warp's base; stable by construction.
+static constexpr int kWarpE = 512;
+__global__ void __launch_bounds__(1024) bk_scatter_blk(const int* __restrict__ ne, int N, int E, const int* __restrict__ off,
+                                                       const int* __restrict__ seg_off, const int* __restrict__ tile_off,
+                                                       int tile_nodes, int* __restrict__ perm, int* __restrict__ tile_perm) {
+  extern __shared__ int cw[];  // [32 warps][E+1]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, E1 = E + 1;
+  for (int x = tid; x < 32 * E1; x += 1024) cw[x] = 0;
+  __syncthreads();
+  const int i = blockIdx.x * kChunk + tid;
+  int e = -1;
+  if (i < N) {
+    e = ne[i];
+    if (e < 0 || e >= E) e = E;
+  }
+  const unsigned peers = __match_any_sync(0xffffffffu, e);
+  const int rank = __popc(peers & ((1u << lane) - 1u));
+  if (e >= 0 && lane == __ffs(peers) - 1) cw[warp * E1 + e] = __popc(peers);
+  __syncthreads();
+  // exclusive scan over warps for each element, seeded with the chunk offset
+  for (int x = tid; x < E1; x += 1024) {
+    int r = off[(size_t)blockIdx.x * E1 + x];
+#pragma unroll 8
+    for (int w = 0; w < 32; w++) {
+      const int c = cw[w * E1 + x];
+      cw[w * E1 + x] = r;
+      r += c;
+    }
+  }
+  __syncthreads();
+  if (e >= 0) {
+    const int pos = cw[warp * E1 + e] + rank;
+    perm[pos] = i;
+    if (e < E) {
+      const int r = pos - seg_off[e];
+      tile_perm[(size_t)(tile_off[e] + r / tile_nodes) * tile_nodes + r % tile_nodes] = i;
+    }
+  }
+}
+
 __global__ void bk_fill_nan(const int* __restrict__ perm, const int* __restrict__ seg_off, int E,
                             float* __restrict__ out, long long row) {
   const int s = seg_off[E], t = seg_off[E + 1];
@@ -164,12 +217,20 @@ int bucket_launch(const BucketArgs& a, cudaStream_t st) {
   const int nchunks = (a.N + kChunk - 1) / kChunk;
   const size_t sm_e = sizeof(int) * (a.E + 1);
   if (a.N > 0) bk_hist<<<nchunks, 256, sm_e, st>>>(a.node_elem, a.N, a.E, a.hist, a.chunk_bad);
-  bk_scan<<<1, 256, 3 * sm_e, st>>>(a.hist, nchunks, a.E, a.off, a.seg_off, a.tiles, a.n_tiles, a.items,
+  if (3 * sm_e > 48 * 1024) cudaFuncSetAttribute(bk_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * sm_e));
+  bk_scan<<<1, 1024, 3 * sm_e, st>>>(a.hist, nchunks, a.E, a.off, a.seg_off, a.tiles, a.n_tiles, a.items,
                                     a.n_items, a.item_off, a.tile_off, a.tile_perm, a.tile_nodes, a.tiles_per_item,
                                     a.chunk_bad, a.err);
-  if (a.N > 0)
-    bk_scatter<<<nchunks, 32, sm_e, st>>>(a.node_elem, a.N, a.E, a.off, a.seg_off, a.tile_off, a.tile_nodes, a.perm,
-                                          a.tile_perm);
+  if (a.N > 0) {
+    if (a.E + 1 <= kWarpE && 32 * sm_e > 48 * 1024)
+      cudaFuncSetAttribute(bk_scatter_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(32 * sm_e));
+    if (a.E + 1 <= kWarpE)
+      bk_scatter_blk<<<nchunks, 1024, 32 * sm_e, st>>>(a.node_elem, a.N, a.E, a.off, a.seg_off, a.tile_off, a.tile_nodes,
+                                                       a.perm, a.tile_perm);
+    else
+      bk_scatter<<<nchunks, 32, sm_e, st>>>(a.node_elem, a.N, a.E, a.off, a.seg_off, a.tile_off, a.tile_nodes, a.perm,
+                                            a.tile_perm);
+  }
   return a.N > 0 ? 3 : 1;
 }
 

@@ -55,6 +55,7 @@ struct KernelConfig {
   bool coef_unroll = false;  // unroll the per-lane cp.async loop of the coefficient staging
   int tile_nodes = 64;       // nodes per tile (= 64 * node_pairs_per_lane; set by the plan)
   int node_pairs_per_lane = 1;  // fwd / dA: node pairs per lane (1 or 2)
+  int acc_split = 1;         // fwd: independent partial accumulators per output (breaks FFMA2 chains)
   bool a_prefetch = true;    // fwd / dA: prefetch the next item's A / dB rows into registers
   int dw_tiles_per_item = 4; // tiles per dW work item
   int dw_tiles_per_butterfly = 2;  // tiles whose products are summed before one cross-lane reduction

@@ -46,12 +46,14 @@ def main():
         sys.path.insert(0, ROOT)
         from bench import ClockSampler
         with ClockSampler(0) as clk:
+            clk.start()
             e0.record()
             for _ in range(args.iters):
                 sc.forward_raw(A, W, ne, B=B)
                 sc.backward_raw(A, W, ne, dB, dA=dA, dW=dW, reuse=True)
             e1.record()
             torch.cuda.synchronize()
+            clk.end()
         prof = _lib.symcon_profile_read(sc.plan)
         _lib.symcon_profile_enable(sc.plan, 0)
         s, bad = sc.check_device_error()
