@@ -64,12 +64,55 @@ __global__ void __launch_bounds__(1024) bk_scan(const int* __restrict__ hist, in
   for (int c = tid; c < nchunks; c += blockDim.x) atomicMin(&bad, chunk_bad[c]);
   __syncthreads();
   if (tid == 0) *err = (bad == 0x7fffffff) ? ~0ull : (unsigned long long)bad;
-  // 2. segment / tile / item offsets (serial over elements, tiny)
-  if (tid == 0) {
+  // 2. segment / tile / item offsets: block-wide exclusive scans of (count, tiles, items) per element
+  if (E1 <= (int)blockDim.x) {
+    __shared__ int wsum[3][32];
+    int c = 0, nt = 0, ni = 0;
+    if (tid < E1) {
+      c = tot[tid];
+      nt = (tid < E) ? (c + tile_nodes - 1) / tile_nodes : 0;
+      ni = (nt + tiles_per_item - 1) / tiles_per_item;
+    }
+    int xc = c, xt = nt, xi = ni;  // inclusive warp scans
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int yc = __shfl_up_sync(0xffffffffu, xc, o), yt = __shfl_up_sync(0xffffffffu, xt, o),
+                yi = __shfl_up_sync(0xffffffffu, xi, o);
+      if (lane >= o) { xc += yc; xt += yt; xi += yi; }
+    }
+    if (lane == 31) { wsum[0][warp] = xc; wsum[1][warp] = xt; wsum[2][warp] = xi; }
+    __syncthreads();
+    if (warp == 0) {
+      int a = wsum[0][lane], b = wsum[1][lane], d = wsum[2][lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int ya = __shfl_up_sync(0xffffffffu, a, o), yb = __shfl_up_sync(0xffffffffu, b, o),
+                  yd = __shfl_up_sync(0xffffffffu, d, o);
+        if (lane >= o) { a += ya; b += yb; d += yd; }
+      }
+      wsum[0][lane] = a; wsum[1][lane] = b; wsum[2][lane] = d;  // inclusive warp totals
+    }
+    __syncthreads();
+    const int bc = warp ? wsum[0][warp - 1] : 0, bt = warp ? wsum[1][warp - 1] : 0, bi = warp ? wsum[2][warp - 1] : 0;
+    __syncthreads();
+    if (tid < E1) {
+      const int sc = bc + xc - c, st2 = bt + xt - nt, si = bi + xi - ni;  // exclusive
+      tot[tid] = sc; seg_off[tid] = sc;
+      toff[tid] = st2; tile_off[tid] = st2;
+      ioff[tid] = si; item_off[tid] = si;
+      if (tid == E) {
+        seg_off[E + 1] = sc + c;
+        tile_off[E] = st2;     // bucket E has no tiles
+        *n_tiles = st2;
+        *n_items = si;
+        item_off[E + 1] = si;
+      }
+    }
+  } else if (tid == 0) {
     int s = 0, ts = 0, is = 0;
     for (int e = 0; e <= E; e++) {
       int c = tot[e];
-      tot[e] = s;          // becomes the segment start
+      tot[e] = s;
       seg_off[e] = s;
       s += c;
       int nt = (e < E) ? (c + tile_nodes - 1) / tile_nodes : 0;
@@ -249,14 +292,15 @@ __global__ void dw_reduce_items(const float* __restrict__ spart, const int* __re
   const long long per = (long long)npad * K;
   if (slot >= per) return;
   const int it0 = item_off[z], it1 = item_off[z + 1];
-  float s = 0.f;
+  // 8 independent partial sums (loads in flight together), combined in a fixed order
+  float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   int it = it0;
-  for (; it + 4 <= it1; it += 4) {
-    const float a = spart[it * per + slot], b = spart[(it + 1) * per + slot];
-    const float c = spart[(it + 2) * per + slot], d = spart[(it + 3) * per + slot];
-    s += a; s += b; s += c; s += d;
+  for (; it + 8 <= it1; it += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; u++) a[u] += spart[(it + u) * per + slot];
   }
-  for (; it < it1; it++) s += spart[it * per + slot];
+  for (int u = 0; it < it1; it++, u++) a[u] += spart[it * per + slot];
+  const float s = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
   stot[(long long)z * per + slot] = s;
 }
 
