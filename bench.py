@@ -353,8 +353,21 @@ def run_ours(args):
                 achieved = per_nc * mean_nodes * K / (avg_ms / 1e3) / 1e12  # T lane-ops/s
                 sm_mhz = 1965.0
                 peak = 148 * 128 * sm_mhz * 1e6 / 1e12
+                nlm = (cfg.lmax_in + 1) ** 2
+                outc = sc.out_dim // K
+                alg_b = {"symcon_fwd": 4 * (nlm + outc), "symcon_bwd_dA": 4 * (2 * nlm + outc),
+                         "symcon_bwd_dW": 4 * (nlm + outc)}[kern] * mean_nodes * K
+                traffic, tsrc = None, None
+                tpath = os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")
+                if os.path.exists(tpath) and args.config == "mp_medium":
+                    tj = json.load(open(tpath))
+                    rec = tj["kernels"].get(kern)
+                    if rec:
+                        traffic = rec["dram_bytes_read"] + rec["dram_bytes_write"]
+                        tsrc = tj["source"]
                 roof = {"bound": "alu", "kernel": kern, "achieved": achieved, "peak": peak, "unit": "Tops/s (fp32 FMA lane-ops)",
-                        "frac": achieved / peak, "traffic": None, "avg_launch_ms": avg_ms,
+                        "frac": achieved / peak, "traffic": traffic, "traffic_source": tsrc,
+                        "algorithmic_bytes": alg_b, "avg_launch_ms": avg_ms,
                         "ops_per_node_channel": per_nc,
                         "peak_derivation": "148 SMs x 128 FP32 lanes x 1965 MHz (clocks.max.sm); FFMA probe measured 36.0 T/s"}
         path_ops = ops["path"] * (nodes / args.steps) * K
