@@ -49,6 +49,7 @@ struct KernelConfig {
   int tile_warps = 2;        // fwd / dA persistent kernels: warps (channels) per CTA
   bool coef_tma = false;     // stage coefficients with cp.async.bulk + mbarrier (else per-lane cp.async)
   int tile_min_blocks = 1;   // __launch_bounds__ min blocks for fwd / dA (caps registers)
+  int coef_batch = 0;        // >0: coefficient LDS in double-buffered batches of this many quads
   int coef_lookahead = 6;    // coefficient quads loaded ahead of first use
   int coef_mode = 0;         // coefficient staging: 0 per-lane cp.async, 2 registers (LDG.128) + STS
   bool coef_volatile = true; // issue coefficient LDS with volatile asm at the lookahead position
