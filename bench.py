@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=4096, help="nodes in the oracle's bounded sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-overlap", action="store_true", help="all-reduce dW after dA instead of overlapping")
+    ap.add_argument("--sequential-bwd", action="store_true", help="run the dW and dA kernels back to back on one stream")
     return ap.parse_args()
 
 
@@ -231,7 +232,6 @@ def run_ours(args):
     from synth.inputs import gen_A, gen_W, gen_dB
     cfg = shape_of(args.config)
     sc = SymmetricContraction(cfg.lmax_in, cfg.correlation, cfg.out_L, cfg.n_elements, cfg.channels, device=local)
-    _lib.symcon_profile_enable(sc.plan, 1)
 
     from paper_2504_10700_b200.dist import BinPackedShards, DataParallelContraction
     from synth.inputs import table2_sizes
@@ -259,7 +259,7 @@ def run_ours(args):
     dW = torch.empty_like(W)
     for q in range(POOL):
         sc.workspace(pool[q][1])
-    dp = DataParallelContraction(sc, overlap=not args.no_overlap)
+    dp = DataParallelContraction(sc, overlap=not args.no_overlap, concurrent_bwd=not args.sequential_bwd)
 
     def step(q):
         b, N, A, ne, dB, B, dA = pool[q % POOL]
@@ -290,7 +290,19 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
+    # per-kernel times for the roofline: a separate pass with the kernels back to back on one
+    # stream (the throughput region above overlaps dW and dA, which would blur each kernel's time)
+    _lib.symcon_profile_enable(sc.plan, 1)
+    _lib.symcon_profile_reset(sc.plan)
+    seq = DataParallelContraction(sc, overlap=not args.no_overlap, concurrent_bwd=False)
+    launches_timed = dp.launches
+    for q in range(args.steps):
+        b_, N_, A_, ne_, dB_, B_, dA_ = pool[q % POOL]
+        seq.forward(A_, W, ne_, B=B_)
+        seq.backward(A_, W, ne_, dB_, dA=dA_, dW=dW)
+    torch.cuda.synchronize()
     prof = _lib.symcon_profile_read(sc.plan)
+    _lib.symcon_profile_enable(sc.plan, 0)
     t = torch.tensor([ms, nodes], dtype=torch.float64, device=dev)
     if world > 1:
         tt = [torch.zeros_like(t) for _ in range(world)]
@@ -388,7 +400,8 @@ def run_ours(args):
             "path_tops": path_ops / (ms_max / args.steps / 1e3) / 1e12,
             "path_frac_of_alu_peak": path_ops / (ms_max / args.steps / 1e3) / 1e12 / (148 * 128 * 1.965e-3),
             "roofline": roof, "kernels": kernels, "alg_ops_per_node_channel": ops,
-            "clocks": clocks, "gpu_launches": dp.launches,
+            "clocks": clocks, "gpu_launches": launches_timed,
+            "kernel_timing": "per-kernel CUDA events from a separate pass of the same steps with dW and dA back to back",
             "e2e": {"value": e2e_value, "unit": "nodes/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "note": "H2D A+node_elem+dB from pinned host, D2H dW, per step through SymmetricContraction"},
         }

@@ -63,6 +63,7 @@ struct KernelConfig {
   int dw_min_blocks = 2;           // __launch_bounds__ min blocks of the dW kernel
   int dw_rows_per_group = 26;      // transposed dW: rows j per warp (register accumulators)
   int dw_groups_per_cta = 16;      // transposed dW: warps per CTA
+  int dw_batch = 1;                // transposed dW: rows whose products are emitted before their FMAs
   int dw_block_nodes = 8;          // transposed dW: nodes per smem stage
   int unfold_channels = 8;   // channels per unfold CTA
 };

@@ -44,10 +44,14 @@ class BinPackedShards:
 
 
 class DataParallelContraction:
-    """Forward + backward of one rank's bin with the dW all-reduce overlapped with dA."""
+    """Forward + backward of one rank's bin. The dW kernels run on the main stream and the dA
+    kernel on a side stream (concurrently; `concurrent_bwd`), and for N > 1 the dW all-reduce
+    runs on a communication stream as soon as dW is ready, overlapped with dA."""
 
-    def __init__(self, sc, group=None, overlap=True):
+    def __init__(self, sc, group=None, overlap=True, concurrent_bwd=True):
         self.sc = sc
+        self.concurrent_bwd = concurrent_bwd
+        self.side = torch.cuda.Stream(device=sc.device) if concurrent_bwd else None
         self.group = group
         self.overlap = overlap
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -61,9 +65,20 @@ class DataParallelContraction:
 
     def backward(self, A, W, node_elem, dB, dA=None, dW=None):
         sc = self.sc
-        if self.world == 1:
+        if self.world == 1 and not self.concurrent_bwd:
             dA, dW = sc.backward_raw(A, W, node_elem, dB, dA=dA, dW=dW, reuse=True)
             self.launches += sc.last_launch_count()
+            return dA, dW
+        if self.world == 1:
+            # dW and dA kernels on two streams (they can share SMs as either drains)
+            main = torch.cuda.current_stream(sc.device)
+            self.side.wait_stream(main)          # inputs ready; dW and dA then run concurrently
+            _, dW = sc.backward_raw(A, W, node_elem, dB, need_dA=False, dW=dW, reuse=True)
+            self.launches += sc.last_launch_count()
+            with torch.cuda.stream(self.side):
+                dA, _ = sc.backward_raw(A, W, node_elem, dB, need_dW=False, dA=dA, reuse=True, ws_key="default")
+                self.launches += sc.last_launch_count()
+            main.wait_stream(self.side)
             return dA, dW
         main = torch.cuda.current_stream(sc.device)
         if not self.overlap:
@@ -71,8 +86,10 @@ class DataParallelContraction:
             self.launches += sc.last_launch_count()
             dist.all_reduce(dW, group=self.group)
             return dA, dW
-        # dW first (bucketing and W-fold reused from the forward), then all-reduce on the comm
-        # stream while the dA kernel runs on the main stream
+        # dW first (bucketing and W-fold reused from the forward), its all-reduce on the comm stream;
+        # dA on a side stream from the start (concurrent with dW and with the all-reduce)
+        if self.concurrent_bwd:
+            self.side.wait_stream(main)
         _, dW = sc.backward_raw(A, W, node_elem, dB, need_dA=False, dW=dW, reuse=True)
         self.launches += sc.last_launch_count()
         ev = torch.cuda.Event()
@@ -81,7 +98,13 @@ class DataParallelContraction:
         with torch.cuda.stream(self.comm):
             dist.all_reduce(dW, group=self.group)
         dW.record_stream(self.comm)
-        dA, _ = sc.backward_raw(A, W, node_elem, dB, need_dW=False, dA=dA, reuse=True)
-        self.launches += sc.last_launch_count()
+        if self.concurrent_bwd:
+            with torch.cuda.stream(self.side):
+                dA, _ = sc.backward_raw(A, W, node_elem, dB, need_dW=False, dA=dA, reuse=True)
+                self.launches += sc.last_launch_count()
+            main.wait_stream(self.side)
+        else:
+            dA, _ = sc.backward_raw(A, W, node_elem, dB, need_dW=False, dA=dA, reuse=True)
+            self.launches += sc.last_launch_count()
         main.wait_stream(self.comm)
         return dA, dW
