@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-overlap", action="store_true", help="all-reduce dW after dA instead of overlapping")
     ap.add_argument("--sequential-bwd", action="store_true", help="run the dW and dA kernels back to back on one stream")
+    ap.add_argument("--concurrent-bwd", action="store_true", help="run dA on a side stream concurrent with dW (default at N=1)")
     return ap.parse_args()
 
 
@@ -259,7 +260,8 @@ def run_ours(args):
     dW = torch.empty_like(W)
     for q in range(POOL):
         sc.workspace(pool[q][1])
-    dp = DataParallelContraction(sc, overlap=not args.no_overlap, concurrent_bwd=not args.sequential_bwd)
+    conc = False if args.sequential_bwd else (True if args.concurrent_bwd else None)
+    dp = DataParallelContraction(sc, overlap=not args.no_overlap, concurrent_bwd=conc)
 
     def step(q):
         b, N, A, ne, dB, B, dA = pool[q % POOL]
