@@ -349,8 +349,8 @@ symcon_status symcon_build_tables(int lmax_in, int correlation, const int* out_L
     {
       const int nout = p->t.out_per_ch, nrows = (int)p->t.rows.size();
       const int ng = (nrows + p->kc.dw_rows_per_group - 1) / p->kc.dw_rows_per_group;  // must match codegen
-      p->dw_gpc = std::min(ng, p->kc.dw_groups_per_cta);
-      p->dw_nz = (ng + p->dw_gpc - 1) / p->dw_gpc;
+      p->dw_nz = (ng + p->kc.dw_groups_per_cta - 1) / p->kc.dw_groups_per_cta;
+      p->dw_gpc = (ng + p->dw_nz - 1) / p->dw_nz;
       p->dw_smem = sizeof(float) * (size_t)p->kc.dw_block_nodes * (p->t.n_lm + nout) * 34;
       if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_dW, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                            (int)p->dw_smem, device), "dW smem attribute");
