@@ -602,7 +602,7 @@ symcon_status symcon_backward_ex(const symcon_plan* p, int64_t N, const float* A
   if (dW) {
     {
     Timed tm(p, K_DW, st);
-    s = cuda_err(cudaLaunchKernel((const void*)p->k_dW, dim3((unsigned)w.max_items, (p->t.K + 31) / 32, p->dw_nz),
+    s = cuda_err(cudaLaunchKernel((const void*)p->k_dW, dim3((unsigned)(w.max_items * p->dw_nz), (p->t.K + 31) / 32, 1),
                                   dim3(32 * p->dw_gpc), args, p->dw_smem, st), "launch symcon_bwd_dW");
     }
     if (s) return s;
