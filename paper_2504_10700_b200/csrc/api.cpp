@@ -294,6 +294,10 @@ static symcon_status build_common(int lmax_in, int corr, const int* out_L, int n
   std::vector<int> ol(out_L, out_L + n_out);
   if (!build_tables(lmax_in, corr, ol, E, K, p->t)) { delete p; return SYMCON_EINVAL; }
   p->npad = (int)((p->t.rows.size() + 31) / 32 * 32);
+  // measured defaults (profiles/r01): few large row groups when the dB row is short (MP-medium:
+  // 52 rows x 8 warps, fewer smem reads per FMA), smaller groups for the 9-output large shape
+  if (p->kc.dw_rows_per_group <= 0) p->kc.dw_rows_per_group = p->t.out_per_ch > 4 ? 26 : 52;
+  if (p->kc.dw_groups_per_cta <= 0) p->kc.dw_groups_per_cta = p->t.out_per_ch > 4 ? 16 : 8;
   p->source = generate_source(p->t, p->kc);
   *out = p;
   return SYMCON_OK;

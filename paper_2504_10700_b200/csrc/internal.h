@@ -61,8 +61,8 @@ struct KernelConfig {
   int dw_tiles_per_item = 4; // tiles per dW work item
   int dw_tiles_per_butterfly = 2;  // tiles whose products are summed before one cross-lane reduction
   int dw_min_blocks = 2;           // __launch_bounds__ min blocks of the dW kernel
-  int dw_rows_per_group = 26;      // transposed dW: rows j per warp (register accumulators)
-  int dw_groups_per_cta = 16;      // transposed dW: warps per CTA
+  int dw_rows_per_group = 0;       // transposed dW: rows j per warp (register accumulators); 0 = auto
+  int dw_groups_per_cta = 0;       // transposed dW: warps per CTA; 0 = auto
   int dw_batch = 1;                // transposed dW: rows whose products are emitted before their FMAs
   int dw_block_nodes = 8;          // transposed dW: nodes per smem stage
   int unfold_channels = 8;   // channels per unfold CTA
