@@ -71,21 +71,31 @@ def bin_elements(sizes, offs, ids, b, n_elements):
 
 
 def alg_ops(sc):
-    """Algorithmic FP32 lane-ops per (node, channel) per kernel, from the plan's tables
-    (DESIGN.md §8): products = distinct (a,b) prefixes + degree-3 monomials; fold = rows;
-    partials = sum over monomials of distinct factors."""
+    """Algorithmic FP32 lane-ops per (node, channel), per kernel and for the whole path, counted
+    from the plan's tables; each is the op count of the exact evaluation the
+    kernel performs, which is the smallest we know (so the roofline stays a bound):
+      fwd  = prefix products (a,b) + degree-3 monomials + folded rows   (monomials, then one FMA per row)
+      dW   = same products + folded rows                                 (S_j += dB_o * mono_j)
+      dA   = prefix products of degree-3 monomials + folded rows (g_j) + 2 per degree-3 monomial
+             + 2 per prefix group + 1 per degree-1 monomial          (reverse of the prefix structure)
+      path = fwd + dA + dW with the backward's products shared."""
     from paper_2504_10700_b200 import _lib
     L, M, mono, col, val = _lib.symcon_plan_sym_table(sc.plan)
     rows = {(int(L[i]), int(M[i]), tuple(int(x) for x in mono[i])) for i in range(len(L))}
     monos = {r[2] for r in rows}
-    prefixes = {m[:2] for m in monos if m[1] >= 0}
-    deg3 = [m for m in monos if m[2] >= 0]
-    products = len(prefixes) + len(deg3)
-    partials = sum(len({x for x in m if x >= 0}) for m in monos)
+    deg = {m: sum(1 for x in m if x >= 0) for m in monos}
+    prefixes = {m[:2] for m in monos if deg[m] >= 2}
+    prefixes3 = {m[:2] for m in monos if deg[m] == 3}
+    deg3 = sum(1 for m in monos if deg[m] == 3)
+    deg1 = sum(1 for m in monos if deg[m] == 1)
     n_fold = len(rows)
-    return {"fwd": products + n_fold, "dA": products + n_fold + partials, "dW": products + n_fold,
-            "path": 2 * products + 3 * n_fold + partials, "n_fold": n_fold, "products": products,
-            "partials": partials, "n_sym": int(len(L))}
+    products = len(prefixes) + deg3
+    fwd = products + n_fold
+    dW = products + n_fold
+    dA = len(prefixes3) + n_fold + 2 * deg3 + 2 * len(prefixes) + deg1
+    path = fwd + (products + n_fold) + (n_fold + 2 * deg3 + 2 * len(prefixes) + deg1)
+    return {"fwd": fwd, "dA": dA, "dW": dW, "path": path, "n_fold": n_fold, "products": products,
+            "prefixes": len(prefixes), "deg3_monomials": deg3, "n_sym": int(len(L))}
 
 
 # ----------------------------------------------------------------------------- clocks
