@@ -46,6 +46,7 @@ bool build_tables(int lmax_in, int corr, const std::vector<int>& out_L, int E, i
 // ---- codegen.cpp
 struct KernelConfig {
   int warps_per_cta = 8;     // dW kernel: channels per CTA (one warp per channel)
+  int tile_sched = 0;        // fwd / dA: 0 strided items, 1 k-major contiguous ranges (coefficient reuse)
   int tile_warps = 1;        // fwd / dA persistent kernels: warps (channels) per CTA
   bool coef_tma = false;     // stage coefficients with cp.async.bulk + mbarrier (else per-lane cp.async)
   int tile_min_blocks = 1;   // __launch_bounds__ min blocks for fwd / dA (caps registers)
