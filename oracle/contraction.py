@@ -145,3 +145,52 @@ def forward_bruteforce(prob, A, W, node_elem):
                 spec = "M" + letters[:p.nu] + "," + ",".join(letters[:p.nu]) + "->M"
                 out[p.L][i, k] += W[z, p.col, k] * np.einsum(spec, U, *([a] * p.nu))
     return np.concatenate([out[L].reshape(N, -1) for L in prob.out_L], axis=1)
+
+
+def backward2(prob, A, W, node_elem, dB, uA):
+    """Double backward: derivatives of <uA, dA(A, W, dB)> w.r.t. A, W and dB (forces in the loss,
+    PAPER.md:331, 967, 1549), from the raw ordered tuples:
+
+        dB_bar[i,k,(L,M)] = sum_{paths} W sum_{nnz} U sum_j uA[t_j] prod_{j' != j} A[t_j']
+        W_bar[z,p,k]      = sum_{i: z_i = z} sum_M dB_M sum_{nnz} U sum_j uA[t_j] prod_{j' != j} A[t_j']
+        A_bar[i,k,b]      = sum_M dB_M sum_{paths} W sum_{nnz} U sum_{j} uA[t_j]
+                            sum_{j'' != j, t_j'' = b} prod_{j' not in {j, j''}} A[t_j']
+    """
+    A = np.asarray(A, dtype=np.float64)
+    W = np.asarray(W, dtype=np.float64)
+    uA = np.asarray(uA, dtype=np.float64)
+    N, K, E = _check(prob, A, W, node_elem)
+    node_elem = np.asarray(node_elem)
+    Wn = W[node_elem]
+    g = _split_out(prob, dB, N, K)
+    dB_bar = {L: np.zeros((N, K, 2 * L + 1)) for L in prob.out_L}
+    A_bar = np.zeros_like(A)
+    W_bar = np.zeros_like(W)
+
+    def prod_except(ts, skip):
+        out = np.ones(A.shape[:2])
+        for jj, t in enumerate(ts):
+            if jj not in skip:
+                out = out * A[:, :, t]
+        return out
+
+    for p in prob.paths:
+        w = Wn[:, p.col, :]
+        Pp = np.zeros((N, K))
+        for M, ts, u in p.terms:
+            gM = g[p.L][:, :, M + p.L]
+            jvp = np.zeros((N, K))                       # sum_j uA[t_j] prod_{j' != j} A
+            for j, t in enumerate(ts):
+                jvp += uA[:, :, t] * prod_except(ts, {j})
+            dB_bar[p.L][:, :, M + p.L] += w * u * jvp
+            Pp += gM * u * jvp
+            for j, t in enumerate(ts):
+                for j2, b in enumerate(ts):
+                    if j2 != j:
+                        A_bar[:, :, b] += gM * w * u * uA[:, :, t] * prod_except(ts, {j, j2})
+        for z in range(E):
+            sel = node_elem == z
+            if sel.any():
+                W_bar[z, p.col, :] = Pp[sel].sum(axis=0)
+    dB_bar = np.concatenate([dB_bar[L].reshape(N, -1) for L in prob.out_L], axis=1)
+    return dB_bar, A_bar, W_bar

@@ -185,3 +185,48 @@ def test_onehot_dB_gives_path_features():
         assert dW[ne[i], p.col, k] == pytest.approx(expect, abs=1e-14)
     others = [z for z in range(W.shape[0]) if z != ne[i]]
     assert np.all(dW[others] == 0)
+
+
+def test_backward2_against_finite_differences():
+    """The double backward is the derivative of <uA, dA(A, W, dB)>: check it by central differences of
+    the (already FD-pinned) backward; dB enters linearly, so its derivative is exact."""
+    from oracle.contraction import backward2
+    prob = Problem(3, 3, [0, 1])
+    for seed in range(6):
+        A, W, ne, rng = _inputs(prob, N=2, K=2, seed=seed)
+        dB = rng.normal(size=(2, prob.out_dim(2)))
+        uA = rng.normal(size=A.shape)
+        dB_bar, A_bar, W_bar = backward2(prob, A, W, ne, dB, uA)
+        f = lambda A_, W_, dB_: (uA * backward(prob, A_, W_, ne, dB_)[0]).sum()
+        h = 1e-6
+        for _ in range(3):
+            idx = tuple(rng.integers(0, s) for s in A.shape)
+            Ap, Am = A.copy(), A.copy()
+            Ap[idx] += h
+            Am[idx] -= h
+            assert (f(Ap, W, dB) - f(Am, W, dB)) / (2 * h) == pytest.approx(A_bar[idx], rel=1e-7, abs=1e-8)
+            idx = tuple(rng.integers(0, s) for s in W.shape)
+            Wp, Wm = W.copy(), W.copy()
+            Wp[idx] += h
+            Wm[idx] -= h
+            assert (f(A, Wp, dB) - f(A, Wm, dB)) / (2 * h) == pytest.approx(W_bar[idx], rel=1e-7, abs=1e-8)
+            idx = tuple(rng.integers(0, s) for s in dB.shape)
+            e = np.zeros_like(dB)
+            e[idx] = 1.0
+            assert f(A, W, e) == pytest.approx(dB_bar[idx], rel=1e-10, abs=1e-12)   # linear in dB
+
+
+def test_backward2_jvp_and_symmetry():
+    """dB_bar is the JVP of the forward in direction uA; <v, A_bar(uA)> = <uA, A_bar(v)> (the
+    dB-weighted Hessian is symmetric)."""
+    from oracle.contraction import backward2
+    prob = Problem(3, 3, [0, 1, 2])
+    A, W, ne, rng = _inputs(prob, N=3, K=2)
+    dB = rng.normal(size=(3, prob.out_dim(2)))
+    u, v = rng.normal(size=A.shape), rng.normal(size=A.shape)
+    dB_bar, Au, _ = backward2(prob, A, W, ne, dB, u)
+    _, Av, _ = backward2(prob, A, W, ne, dB, v)
+    h = 1e-6
+    jvp = (forward(prob, A + h * u, W, ne) - forward(prob, A - h * u, W, ne)) / (2 * h)
+    assert np.allclose(jvp, dB_bar, rtol=1e-7, atol=1e-8)
+    assert (v * Au).sum() == pytest.approx((u * Av).sum(), rel=1e-11)
