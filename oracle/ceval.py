@@ -86,3 +86,16 @@ class OracleC:
         self.lib.oracle_backward(ctypes.byref(self.t), ctypes.c_int64(N), ctypes.c_int64(K), ctypes.c_int64(E),
                                  p(A), p(W), p(ne), p(dB), p(dA), p(dW))
         return dA, dW
+
+    def backward2(self, A, W, node_elem, dB, uA, want_dB=True, want_A=True, want_W=True):
+        A, W, dB, uA = self._f32(A), self._f32(W), self._f32(dB), self._f32(uA)
+        ne = np.ascontiguousarray(node_elem, dtype=np.int32)
+        N, K, _ = A.shape
+        E = W.shape[0]
+        dBb = np.zeros((N, self.prob.out_dim(K))) if want_dB else None
+        Ab = np.zeros(A.shape) if want_A else None
+        Wb = np.zeros(W.shape) if want_W else None
+        p = lambda x: x.ctypes.data_as(ctypes.c_void_p) if x is not None else None
+        self.lib.oracle_backward2(ctypes.byref(self.t), ctypes.c_int64(N), ctypes.c_int64(K), ctypes.c_int64(E),
+                                  p(A), p(W), p(ne), p(dB), p(uA), p(dBb), p(Ab), p(Wb))
+        return dBb, Ab, Wb

@@ -117,3 +117,71 @@ void oracle_backward(const oracle_tables* T, int64_t N, int64_t K, int64_t E, co
     free(priv);
   }
 }
+
+/* Double backward (oracle/contraction.py:backward2): derivatives of <uA, dA(A, W, dB)> with
+ * respect to dB (dB_bar [N][out_dim]), A (A_bar [N][K][n_lm]) and W (W_bar [E][P][K]); all
+ * overwritten, any may be NULL. Per raw term t with product prod_j a[t_j]:
+ *   jvp = sum_j uA[t_j] prod_{j' != j} a[t_j']
+ *   dB_bar[out(t)] += w u jvp;  W_bar[z, col] += g u jvp
+ *   A_bar[t_j2]    += g w u uA[t_j] prod_{j' not in {j, j2}} a[t_j']   (j != j2) */
+void oracle_backward2(const oracle_tables* T, int64_t N, int64_t K, int64_t E, const float* A,
+                      const float* W, const int32_t* node_elem, const float* dB, const float* uA,
+                      double* dB_bar, double* A_bar, double* W_bar) {
+  const int64_t wsz = E * T->n_paths * K;
+  const int64_t out_dim = T->out_per_ch * K;
+  int nth = oracle_num_threads();
+  double* priv = NULL;
+  if (W_bar) priv = (double*)calloc((size_t)nth * (size_t)wsz, sizeof(double));
+#pragma omp parallel
+  {
+    int tid = 0;
+#ifdef _OPENMP
+    tid = omp_get_thread_num();
+#endif
+    double* myW = priv ? priv + (size_t)tid * wsz : NULL;
+    int64_t i;
+#pragma omp for schedule(dynamic, 16)
+    for (i = 0; i < N; i++) {
+      const int64_t z = node_elem[i];
+      if (A_bar) memset(A_bar + i * K * T->n_lm, 0, sizeof(double) * K * T->n_lm);
+      if (dB_bar) memset(dB_bar + i * out_dim, 0, sizeof(double) * out_dim);
+      for (int64_t k = 0; k < K; k++) {
+        const float* a = A + (i * K + k) * T->n_lm;
+        const float* ua = uA + (i * K + k) * T->n_lm;
+        double* ab = A_bar ? A_bar + (i * K + k) * T->n_lm : NULL;
+        for (int64_t t = 0; t < T->n_terms; t++) {
+          const int64_t o = i * out_dim + T->blk[t] * K + k * T->wid[t] + T->mpos[t];
+          double g = (double)dB[o];
+          double w = (double)W[(z * T->n_paths + T->col[t]) * K + k];
+          int nu = T->nu[t];
+          const int32_t* tp = T->tup + 3 * t;
+          double jvp = 0.0;
+          for (int j = 0; j < nu; j++) {
+            double part = (double)ua[tp[j]];
+            for (int jj = 0; jj < nu; jj++)
+              if (jj != j) part *= (double)a[tp[jj]];
+            jvp += part;
+          }
+          if (dB_bar) dB_bar[o] += w * T->u[t] * jvp;
+          if (myW) myW[(z * T->n_paths + T->col[t]) * K + k] += g * T->u[t] * jvp;
+          if (ab) {
+            for (int j = 0; j < nu; j++)
+              for (int j2 = 0; j2 < nu; j2++) {
+                if (j2 == j) continue;
+                double part = g * w * T->u[t] * (double)ua[tp[j]];
+                for (int jj = 0; jj < nu; jj++)
+                  if (jj != j && jj != j2) part *= (double)a[tp[jj]];
+                ab[tp[j2]] += part;
+              }
+          }
+        }
+      }
+    }
+  }
+  if (W_bar) {
+    memset(W_bar, 0, sizeof(double) * wsz);
+    for (int t = 0; t < nth; t++)
+      for (int64_t x = 0; x < wsz; x++) W_bar[x] += priv[(size_t)t * wsz + x];
+    free(priv);
+  }
+}

@@ -21,3 +21,21 @@ def test_ceval_matches_python():
         dAc, dWc = oc.backward(A, W, ne, dB)
         assert np.abs(dAc - dA).max() <= 1e-13 * np.abs(dA).max()
         assert np.abs(dWc - dW).max() <= 1e-13 * np.abs(dW).max()
+
+
+def test_ceval_backward2_matches_python():
+    from oracle.contraction import backward2
+    for out_L, corr in (((0, 1), 3), ((0, 1, 2), 3), ((1,), 2)):
+        prob = Problem(3, corr, out_L)
+        oc = OracleC(prob)
+        rng = np.random.default_rng(11)
+        N, K, E = 12, 3, 3
+        A = rng.normal(size=(N, K, 16)).astype(np.float32)
+        W = rng.normal(size=(E, prob.n_paths, K)).astype(np.float32)
+        ne = rng.integers(0, E, N).astype(np.int32)
+        dB = rng.normal(size=(N, prob.out_dim(K))).astype(np.float32)
+        uA = rng.normal(size=A.shape).astype(np.float32)
+        ref = backward2(prob, A, W, ne, dB, uA)
+        got = oc.backward2(A, W, ne, dB, uA)
+        for r, g in zip(ref, got):
+            assert np.abs(g - r).max() <= 1e-13 * np.abs(r).max()
