@@ -124,6 +124,23 @@ symcon_status symcon_backward_ex(const symcon_plan* plan, int64_t num_nodes, con
                                  float* dW, void* ws, size_t ws_bytes, uint32_t flags,
                                  void* stream /* cudaStream_t */);
 
+/* Double backward: training on forces differentiates the backward
+ * itself (forces F = -dE/dr enter the loss; MACE trains on energies and
+ * forces). Given the cotangent uA [N][K][n_lm] of dA, returns the derivatives of
+ * <uA, dA(A, W, dB)>:
+ *   dB_bar [N][out_dim]   = sum_paths W U (grad_A monomial . uA)      (the JVP of the forward)
+ *   A_bar  [N][K][n_lm]   = sum_M dB_M sum_paths W U Hess_A(monomial) uA
+ *   W_bar  [E][P][K]      = sum_{i of element z} sum_M dB_M U (grad_A monomial . uA)
+ * (raw-tuple definitions: oracle/contraction.py backward2). Each output is overwritten and may
+ * be NULL to skip it; W_bar of elements without nodes is 0. A, dB, uA, dB_bar and A_bar must be
+ * 16-byte aligned; same shapes, workspace, flags (SYMCON_REUSE_*) and error behaviour as
+ * symcon_backward_ex. The cotangent of dW (uW) needs no kernel of its own: its terms are
+ * symcon_forward (dB_bar += forward(A, uW)) and symcon_backward dA (A_bar += dA(A, uW, dB)). */
+symcon_status symcon_backward2(const symcon_plan* plan, int64_t num_nodes, const float* A,
+                               const float* W, const int32_t* node_elem, const float* dB,
+                               const float* uA, float* dB_bar, float* A_bar, float* W_bar, void* ws,
+                               size_t ws_bytes, uint32_t flags, void* stream /* cudaStream_t */);
+
 /* Synchronises `stream`; returns SYMCON_EELEMENT and *first_bad_node if the last forward /
  * backward that used `ws` saw an out-of-range node_elem, SYMCON_ECUDA on a CUDA error. */
 symcon_status symcon_check_device_error(const symcon_plan* plan, void* ws, void* stream,
@@ -133,9 +150,10 @@ symcon_status symcon_check_device_error(const symcon_plan* plan, void* ws, void*
 int32_t symcon_last_launch_count(const symcon_plan* plan);
 
 /* Optional launch timer for benchmarking: when enabled, every launch group (bucket, fold,
- * fwd, bwd_dA, bwd_dW, unfold, fill_nan) is bracketed by CUDA events on its stream.
- * symcon_profile_read synchronises those events and returns up to 8 entries of
+ * fwd, bwd_dA, bwd_dW, unfold, bwd2, bwd2_dW) is bracketed by CUDA events on its stream.
+ * symcon_profile_read synchronises those events and returns up to SYMCON_PROFILE_MAX entries of
  * (kernel name, launches, total milliseconds); names point to static strings. */
+#define SYMCON_PROFILE_MAX 12
 symcon_status symcon_profile_enable(const symcon_plan* plan, int on);
 symcon_status symcon_profile_reset(const symcon_plan* plan);
 int32_t symcon_profile_read(const symcon_plan* plan, const char** names, int64_t* counts, double* total_ms);

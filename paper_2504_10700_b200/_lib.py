@@ -20,7 +20,7 @@ lib = ctypes.CDLL(LIB_PATH)
 SYMCON_OK, SYMCON_EINVAL, SYMCON_EUNSUPPORTED, SYMCON_ECUDA, SYMCON_ENOMEM, SYMCON_EELEMENT = range(6)
 
 EXPORTS = ["symcon_build_tables", "symcon_plan_info", "symcon_plan_path", "symcon_plan_sym_table", "symcon_real_cg",
-           "symcon_workspace_bytes", "symcon_forward", "symcon_backward", "symcon_backward_ex", "symcon_check_device_error",
+           "symcon_workspace_bytes", "symcon_forward", "symcon_backward", "symcon_backward_ex", "symcon_backward2", "symcon_check_device_error",
            "symcon_last_launch_count", "symcon_destroy", "symcon_status_string", "symcon_last_error",
            "symcon_pack_balanced", "symcon_precompile", "symcon_plan_source", "symcon_profile_enable",
            "symcon_profile_reset", "symcon_profile_read"]
@@ -47,6 +47,7 @@ lib.symcon_workspace_bytes.restype = _sz
 lib.symcon_forward.argtypes = [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
 lib.symcon_backward.argtypes = [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
 lib.symcon_backward_ex.argtypes = [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, ctypes.c_uint32, _vp]
+lib.symcon_backward2.argtypes = [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, ctypes.c_uint32, _vp]
 SYMCON_REUSE_BUCKETS, SYMCON_REUSE_FOLD = 1, 2
 lib.symcon_check_device_error.argtypes = [_vp, _vp, _vp, ctypes.POINTER(_i64)]
 lib.symcon_last_launch_count.argtypes = [_vp]
@@ -67,9 +68,12 @@ lib.symcon_profile_read.argtypes = [_vp, ctypes.POINTER(ctypes.c_char_p), ctypes
                                     ctypes.POINTER(ctypes.c_double)]
 lib.symcon_profile_read.restype = _i32
 for _n in ("symcon_profile_enable", "symcon_profile_reset", "symcon_build_tables", "symcon_plan_info", "symcon_plan_path", "symcon_plan_sym_table", "symcon_real_cg",
-           "symcon_forward", "symcon_backward", "symcon_backward_ex", "symcon_check_device_error", "symcon_pack_balanced",
+           "symcon_forward", "symcon_backward", "symcon_backward_ex", "symcon_backward2", "symcon_check_device_error", "symcon_pack_balanced",
            "symcon_precompile"):
     getattr(lib, _n).restype = ctypes.c_int
+
+
+PROFILE_MAX = 12  # SYMCON_PROFILE_MAX
 
 
 class SymconError(RuntimeError):
@@ -151,6 +155,11 @@ def symcon_backward_ex(plan, num_nodes, A, W, node_elem, dB, dA, dW, ws, ws_byte
           "symcon_backward_ex")
 
 
+def symcon_backward2(plan, num_nodes, A, W, node_elem, dB, uA, dB_bar, A_bar, W_bar, ws, ws_bytes, flags, stream):
+    check(lib.symcon_backward2(plan, num_nodes, A, W, node_elem, dB, uA, dB_bar, A_bar, W_bar, ws, ws_bytes, flags, stream),
+          "symcon_backward2")
+
+
 def symcon_check_device_error(plan, ws, stream):
     bad = _i64(-1)
     s = lib.symcon_check_device_error(plan, ws, stream, ctypes.byref(bad))
@@ -198,8 +207,8 @@ def symcon_profile_reset(plan):
 
 def symcon_profile_read(plan):
     """{kernel name: (launches, total ms)} of the launch timer (synchronises)."""
-    names = (ctypes.c_char_p * 8)()
-    counts = (_i64 * 8)()
-    ms = (ctypes.c_double * 8)()
+    names = (ctypes.c_char_p * PROFILE_MAX)()
+    counts = (_i64 * PROFILE_MAX)()
+    ms = (ctypes.c_double * PROFILE_MAX)()
     n = lib.symcon_profile_read(plan, names, counts, ms)
     return {names[i].decode(): (int(counts[i]), float(ms[i])) for i in range(n)}

@@ -33,12 +33,13 @@ struct symcon_plan {
   KernelConfig kc;
   int device = -1;
   int npad = 0;
-  size_t unfold_smem = 0, tile_smem = 0, dw_smem = 0;
+  size_t unfold_smem = 0, tile_smem = 0, dw_smem = 0, dw2_smem = 0;
   int dw_gpc = 1, dw_nz = 1;
-  int grid_fwd = 0, grid_dA = 0;
+  int grid_fwd = 0, grid_dA = 0, grid_bwd2 = 0;
   std::string source;
   cudaLibrary_t lib = nullptr;
   cudaKernel_t k_fold = nullptr, k_fwd = nullptr, k_dA = nullptr, k_dW = nullptr, k_unfold = nullptr;
+  cudaKernel_t k_bwd2 = nullptr, k_bwd2_dW = nullptr;
   mutable std::atomic<int> last_launches{0};
   // optional launch timer (symcon_profile_*): CUDA events around each launch group
   struct Rec { int kind; cudaEvent_t a, b; };
@@ -46,8 +47,8 @@ struct symcon_plan {
   mutable bool prof_on = false;
   mutable std::vector<Rec> recs;
   mutable std::vector<cudaEvent_t> event_pool;
-  mutable double prof_ms[8] = {0};
-  mutable int64_t prof_n[8] = {0};
+  mutable double prof_ms[SYMCON_PROFILE_MAX] = {0};
+  mutable int64_t prof_n[SYMCON_PROFILE_MAX] = {0};
   // per-workspace record of what the last call left in it (for the SYMCON_REUSE_* hints)
   struct WsState { int64_t N = -1; const void* ne = nullptr; const void* W = nullptr; };
   mutable std::mutex ws_mu;
@@ -55,8 +56,9 @@ struct symcon_plan {
 };
 
 static const char* kKindNames[] = {"symcon_bucket", "symcon_fold", "symcon_fwd", "symcon_bwd_dA", "symcon_bwd_dW",
-                                   "symcon_unfold", "symcon_fill_nan", "other"};
-enum { K_BUCKET = 0, K_FOLD, K_FWD, K_DA, K_DW, K_UNFOLD, K_NAN };
+                                   "symcon_unfold", "symcon_fill_nan", "symcon_bwd2", "symcon_bwd2_dW"};
+enum { K_BUCKET = 0, K_FOLD, K_FWD, K_DA, K_DW, K_UNFOLD, K_NAN, K_BWD2, K_BWD2_DW, K_NKINDS };
+static_assert(K_NKINDS <= SYMCON_PROFILE_MAX, "profile table");
 
 namespace {
 cudaEvent_t take_event(const symcon_plan* p) {
@@ -107,6 +109,7 @@ struct Params {  // must match SymconParams in codegen.cpp
   float zero;
   const int* tile_perm;
   float* stot;
+  const float* U;
 };
 
 struct WsLayout {
@@ -335,11 +338,15 @@ symcon_status symcon_build_tables(int lmax_in, int correlation, const int* out_L
     if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_dA, p->lib, "symcon_bwd_dA"), "get symcon_bwd_dA");
     if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_dW, p->lib, "symcon_bwd_dW"), "get symcon_bwd_dW");
     if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_unfold, p->lib, "symcon_unfold"), "get symcon_unfold");
+    if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_bwd2, p->lib, "symcon_bwd2"), "get symcon_bwd2");
+    if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_bwd2_dW, p->lib, "symcon_bwd2_dW"), "get symcon_bwd2_dW");
     p->tile_smem = sizeof(float) * (size_t)p->kc.tile_warps * (2 * (size_t)p->npad) + 16 * (size_t)p->kc.tile_warps;
     if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                          (int)p->tile_smem, device), "fwd smem attribute");
     if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_dA, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                          (int)p->tile_smem, device), "dA smem attribute");
+    if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_bwd2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         (int)p->tile_smem, device), "bwd2 smem attribute");
     if (!s) {
       int sms = 0, occ_f = 0, occ_a = 0;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -347,6 +354,10 @@ symcon_status symcon_build_tables(int lmax_in, int correlation, const int* out_L
                                                                  p->tile_smem), "occupancy fwd");
       if (!s) s = cuda_err(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, (const void*)p->k_dA, 32 * p->kc.tile_warps,
                                                                          p->tile_smem), "occupancy dA");
+      int occ_2 = 0;
+      if (!s) s = cuda_err(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_2, (const void*)p->k_bwd2, 32 * p->kc.tile_warps,
+                                                                         p->tile_smem), "occupancy bwd2");
+      p->grid_bwd2 = sms * std::max(occ_2, 1);
       p->grid_fwd = sms * std::max(occ_f, 1);
       p->grid_dA = sms * std::max(occ_a, 1);
     }
@@ -358,6 +369,9 @@ symcon_status symcon_build_tables(int lmax_in, int correlation, const int* out_L
       p->dw_smem = sizeof(float) * (size_t)p->kc.dw_block_nodes * (p->t.n_lm + nout) * 34;
       if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_dW, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                            (int)p->dw_smem, device), "dW smem attribute");
+      p->dw2_smem = sizeof(float) * (size_t)p->kc.dw_block_nodes * (2 * p->t.n_lm + nout) * 34;
+      if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_bwd2_dW, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                           (int)p->dw2_smem, device), "bwd2_dW smem attribute");
     }
     p->unfold_smem = sizeof(float) * 32 * (size_t)(p->npad + 1);
     if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_unfold, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -630,6 +644,67 @@ symcon_status symcon_backward_ex(const symcon_plan* p, int64_t N, const float* A
   return cuda_err(cudaGetLastError(), "backward launch");
 }
 
+symcon_status symcon_backward2(const symcon_plan* p, int64_t N, const float* A, const float* W, const int32_t* ne,
+                               const float* dB, const float* uA, float* dB_bar, float* A_bar, float* W_bar, void* ws,
+                               size_t ws_bytes, uint32_t flags, void* stream) {
+  if (!p) { set_error("plan is NULL"); return SYMCON_EINVAL; }
+  cudaStream_t st = (cudaStream_t)stream;
+  p->last_launches = 0;
+  if (N == 0) {
+    if (W_bar) return cuda_err(cudaMemsetAsync(W_bar, 0, sizeof(float) * (size_t)p->t.E * p->t.paths.size() * p->t.K, st), "memset W_bar");
+    return SYMCON_OK;
+  }
+  symcon_status s = check_common(p, N, A, W, ne, ws, ws_bytes);
+  if (s) return s;
+  if (!dB || !aligned16(dB)) { set_error("dB must be non-NULL and 16-byte aligned"); return SYMCON_EINVAL; }
+  if (!uA || !aligned16(uA)) { set_error("uA must be non-NULL and 16-byte aligned"); return SYMCON_EINVAL; }
+  if ((dB_bar && !aligned16(dB_bar)) || (A_bar && !aligned16(A_bar))) {
+    set_error("dB_bar and A_bar must be 16-byte aligned");
+    return SYMCON_EINVAL;
+  }
+  if (!dB_bar && !A_bar && !W_bar) return SYMCON_OK;
+  WsLayout w = layout(p, N);
+  Params q;
+  fill_params(p, w, (char*)ws, N, q);
+  q.A = A;
+  q.W = W;
+  q.node_elem = ne;
+  q.dB = dB;
+  q.U = uA;
+  q.B = dB_bar;
+  q.dA = A_bar;
+  q.dW = W_bar;
+  const bool tile = dB_bar || A_bar;
+  int n = launch_prep(p, w, (char*)ws, N, ne, W, q, st, tile, &s, flags);
+  if (s) return s;
+  void* args[] = {&q};
+  if (W_bar) {
+    {
+      Timed tm(p, K_BWD2_DW, st);
+      s = cuda_err(cudaLaunchKernel((const void*)p->k_bwd2_dW, dim3((unsigned)(w.max_items * p->dw_nz), (p->t.K + 31) / 32, 1),
+                                    dim3(32 * p->dw_gpc), args, p->dw2_smem, st), "launch symcon_bwd2_dW");
+    }
+    if (s) return s;
+    Timed tm(p, K_UNFOLD, st);
+    n += reduce_items_launch(q.spart, q.item_off, p->t.E, p->npad, p->t.K, q.stot, st);
+    s = cuda_err(cudaLaunchKernel((const void*)p->k_unfold, dim3(p->t.E, (p->t.K + 31) / 32), dim3(512), args,
+                                  p->unfold_smem, st), "launch symcon_unfold");
+    if (s) return s;
+    n += 2;
+  }
+  if (tile) {
+    {
+      Timed tm(p, K_BWD2, st);
+      s = cuda_err(cudaLaunchKernel((const void*)p->k_bwd2, dim3(p->grid_bwd2), dim3(32 * p->kc.tile_warps), args, p->tile_smem, st),
+                   "launch symcon_bwd2");
+    }
+    if (s) return s;
+    n++;
+  }
+  p->last_launches = n;
+  return cuda_err(cudaGetLastError(), "backward2 launch");
+}
+
 symcon_status symcon_check_device_error(const symcon_plan* p, void* ws, void* stream, int64_t* first_bad) {
   if (!p || !ws) { set_error("NULL argument"); return SYMCON_EINVAL; }
   cudaStream_t st = (cudaStream_t)stream;
@@ -659,17 +734,17 @@ symcon_status symcon_profile_reset(const symcon_plan* p) {
   if (!p) return SYMCON_EINVAL;
   std::lock_guard<std::mutex> g(p->prof_mu);
   drain(p);
-  for (int i = 0; i < 8; i++) { p->prof_ms[i] = 0; p->prof_n[i] = 0; }
+  for (int i = 0; i < SYMCON_PROFILE_MAX; i++) { p->prof_ms[i] = 0; p->prof_n[i] = 0; }
   return SYMCON_OK;
 }
 
-/* Synchronises the recorded events; fills up to 8 (name, launches, total ms) entries. */
+/* Synchronises the recorded events; fills up to SYMCON_PROFILE_MAX (name, launches, total ms) entries. */
 int32_t symcon_profile_read(const symcon_plan* p, const char** names, int64_t* counts, double* total_ms) {
   if (!p) return 0;
   std::lock_guard<std::mutex> g(p->prof_mu);
   drain(p);
   int n = 0;
-  for (int i = 0; i < 8; i++)
+  for (int i = 0; i < K_NKINDS; i++)
     if (p->prof_n[i]) {
       if (names) names[n] = kKindNames[i];
       if (counts) counts[n] = p->prof_n[i];

@@ -2,7 +2,9 @@
 
     sc = SymmetricContraction(lmax_in=3, correlation=3, out_L=(0, 1), num_elements=89,
                               channels=128, device=0)
-    B = sc(A, W, node_elem)          # autograd-aware; backward gives dA and dW
+    B = sc(A, W, node_elem)          # autograd-aware; backward gives dA and dW, and with
+                                     # create_graph=True the backward is differentiable again
+                                     # (double backward for force training, symcon_backward2)
 
 Every numeric step (bucketing, W-fold, forward, dA, dW, reductions) runs in the CUDA
 kernels of libsymcon.so through the C ABI; tensors only provide pointers.
@@ -95,6 +97,23 @@ class SymmetricContraction:
                                 ws.data_ptr(), ws.numel(), flags, _stream_ptr(self.device))
         return (dA if need_dA else None), (dW if need_dW else None)
 
+    def backward2_raw(self, A, W, node_elem, dB, uA, need_dB=True, need_A=True, need_W=True, ws_key="default",
+                      reuse=False):
+        """Double backward: (dB_bar, A_bar, W_bar) = derivatives of <uA, dA(A, W, dB)> (symcon_backward2)."""
+        N = self._check(A, W, node_elem)
+        assert dB.dtype == torch.float32 and dB.is_contiguous() and dB.shape == (N, self.out_dim)
+        assert uA.dtype == torch.float32 and uA.is_contiguous() and uA.shape == A.shape
+        dBb = torch.empty_like(dB) if need_dB else None
+        Ab = torch.empty_like(A) if need_A else None
+        Wb = torch.empty_like(W) if need_W else None
+        ws = self.workspace(N, ws_key)
+        flags = (_lib.SYMCON_REUSE_BUCKETS | _lib.SYMCON_REUSE_FOLD) if reuse else 0
+        ptr = lambda x: x.data_ptr() if x is not None else None
+        _lib.symcon_backward2(self.plan, N, A.data_ptr(), W.data_ptr(), node_elem.data_ptr(), dB.data_ptr(),
+                              uA.data_ptr(), ptr(dBb), ptr(Ab), ptr(Wb), ws.data_ptr(), ws.numel(), flags,
+                              _stream_ptr(self.device))
+        return dBb, Ab, Wb
+
     def check_device_error(self, ws_key="default"):
         ws = self._ws.get(ws_key)
         if ws is None:
@@ -119,6 +138,41 @@ class _SymconFn(torch.autograd.Function):
     @staticmethod
     def backward(ctx, dB):
         A, W, node_elem = ctx.saved_tensors
+        if torch.is_grad_enabled():
+            # create_graph=True (training on forces): the backward is itself differentiable
+            dA, dW = _SymconBwdFn.apply(A, W, node_elem, dB, ctx.sc)
+            return dA, dW, None, None
         dA, dW = ctx.sc.backward_raw(A, W, node_elem, dB.contiguous(), ctx.needs_input_grad[0], ctx.needs_input_grad[1],
                                      reuse=True)
         return dA, dW, None, None
+
+
+class _SymconBwdFn(torch.autograd.Function):
+    """(A, W, dB) -> (dA, dW) with its own backward: the uA terms run in symcon_backward2; the uW
+    terms are the forward (dB_bar += B(A, uW)) and the dA backward (A_bar += dA(A, uW, dB))."""
+
+    @staticmethod
+    def forward(ctx, A, W, node_elem, dB, sc):
+        ctx.sc = sc
+        A, W, node_elem, dB = A.contiguous(), W.contiguous(), node_elem.contiguous(), dB.contiguous()
+        ctx.save_for_backward(A, W, node_elem, dB)
+        return sc.backward_raw(A, W, node_elem, dB)
+
+    @staticmethod
+    @torch.autograd.function.once_differentiable
+    def backward(ctx, uA, uW):
+        A, W, node_elem, dB = ctx.saved_tensors
+        sc = ctx.sc
+        need_A, need_W, need_dB = ctx.needs_input_grad[0], ctx.needs_input_grad[1], ctx.needs_input_grad[3]
+        A_bar = W_bar = dB_bar = None
+        if uA is not None and (need_A or need_W or need_dB):
+            dB_bar, A_bar, W_bar = sc.backward2_raw(A, W, node_elem, dB, uA.contiguous(), need_dB, need_A, need_W)
+        if uW is not None and (need_A or need_dB):
+            uW = uW.contiguous()
+            if need_dB:
+                f = sc.forward_raw(A, uW, node_elem)
+                dB_bar = f if dB_bar is None else dB_bar.add_(f)
+            if need_A:
+                a, _ = sc.backward_raw(A, uW, node_elem, dB, need_dW=False)
+                A_bar = a if A_bar is None else A_bar.add_(a)
+        return A_bar, W_bar, None, dB_bar, None

@@ -37,6 +37,8 @@ def test_invalid_arguments(L):
     plan = L.symcon_build_tables(3, 3, [0], 2, 8, -1)
     with pytest.raises(L.SymconError):   # host-only plan cannot compute
         L.symcon_forward(plan, 4, 16, 16, 16, 16, 16, 1 << 20, None)
+    with pytest.raises(L.SymconError):
+        L.symcon_backward2(plan, 4, 16, 16, 16, 16, 16, 16, 16, 16, 16, 1 << 20, 0, None)
     L.symcon_destroy(plan)
 
 
@@ -85,7 +87,8 @@ def test_survey_counts(L):
 def test_generated_source_is_straight_line(L):
     plan = L.symcon_build_tables(3, 3, [0, 1], 1, 1, -1)
     src = L.symcon_plan_source(plan)
-    for k in ("symcon_fold", "symcon_fwd", "symcon_bwd_dA", "symcon_bwd_dW", "symcon_unfold"):
+    for k in ("symcon_fold", "symcon_fwd", "symcon_bwd_dA", "symcon_bwd_dW", "symcon_unfold", "symcon_bwd2",
+              "symcon_bwd2_dW"):
         assert f"void __launch_bounds__" in src and k in src
     assert src.count("fma2(") > 300
     L.symcon_destroy(plan)

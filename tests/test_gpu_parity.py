@@ -294,3 +294,105 @@ def test_sharded_dp_step_matches_single_pass():
     torch.cuda.synchronize()
     s = dWs[0] + dWs[1]
     assert (s - dWu).abs().max().item() <= 1e-5 * dWu.abs().max().item()
+
+
+# ---------------------------------------------------------------- double backward (§8(f) row 1)
+def _uA(sc, N, seed):
+    from synth.inputs import gen_A
+    return gen_A(N, sc.channels, sc.n_lm, "cuda", seed + 1000)
+
+
+def test_backward2_tiny_against_python_oracle():
+    from oracle.contraction import Problem, backward2
+    sc = _sc(3, 3, (0, 1), 3, 16)
+    A, W, ne, dB = _inputs(sc, 70)
+    uA = _uA(sc, 70, 0)
+    got = sc.backward2_raw(A, W, ne, dB, uA)
+    torch.cuda.synchronize()
+    ref = backward2(Problem(3, 3, (0, 1)), *_host(A, W, ne, dB, uA))
+    for g, r in zip(got, ref):
+        assert _rel(g.cpu(), r) < TOL
+
+
+@pytest.mark.parametrize("name,lmax,corr,outs,E,K,N,dist", [
+    ("off_small_shape", 3, 3, (0,), 10, 96, 2000, "organic"),
+    ("mp_shape", 3, 3, (0, 1), 89, 128, 2000, "zipf"),
+    ("large_shape", 3, 3, (0, 1, 2), 89, 256, 400, "zipf"),
+    ("ragged_K13", 3, 3, (0, 1), 5, 13, 777, "uniform"),
+    ("lmax2", 2, 3, (0, 1), 4, 24, 500, "uniform"),
+    ("corr1_all_L", 3, 1, (0, 1, 2, 3), 3, 16, 300, "uniform"),
+    ("corr2", 3, 2, (0, 1), 3, 16, 300, "uniform"),
+    ("out_1o_only", 3, 3, (1,), 7, 32, 500, "zipf"),
+])
+def test_backward2_against_c_oracle(name, lmax, corr, outs, E, K, N, dist):
+    from oracle.contraction import Problem
+    from oracle.ceval import OracleC
+    sc = _sc(lmax, corr, outs, E, K)
+    A, W, ne, dB = _inputs(sc, N, dist, seed=5)
+    uA = _uA(sc, N, 5)
+    got = sc.backward2_raw(A, W, ne, dB, uA)
+    torch.cuda.synchronize()
+    assert sc.check_device_error()[0] == 0
+    ref = OracleC(Problem(lmax, corr, outs)).backward2(*_host(A, W, ne, dB, uA))
+    for what, g, r in zip(("dB_bar", "A_bar", "W_bar"), got, ref):
+        if np.abs(r).max() == 0:          # corr1: the map is linear in A, A_bar = 0 exactly
+            assert torch.count_nonzero(g) == 0, (name, what)
+        else:
+            assert _rel(g.cpu(), r) < TOL, (name, what)
+
+
+def test_backward2_subsets_edges_and_bad_elements():
+    from paper_2504_10700_b200 import _lib
+    sc = _sc(3, 3, (0, 1), 6, 16)
+    A, W, ne, dB = _inputs(sc, 129)
+    uA = _uA(sc, 129, 0)
+    full = sc.backward2_raw(A, W, ne, dB, uA)
+    for mask in ((True, False, False), (False, True, False), (False, False, True)):
+        part = sc.backward2_raw(A, W, ne, dB, uA, *mask)
+        for m, f, p in zip(mask, full, part):
+            assert (p is None) != m and (p is None or torch.equal(p, f))
+    # elements without nodes: W_bar = 0; N = 0 overwrites W_bar with zeros
+    ne2 = torch.full_like(ne, 4)
+    _, _, Wb = sc.backward2_raw(A, W, ne2, dB, uA)
+    for z in (0, 1, 2, 3, 5):
+        assert torch.count_nonzero(Wb[z]) == 0
+    e = lambda *s: torch.zeros(s, device="cuda")
+    _, _, Wb = sc.backward2_raw(e(0, 16, 16), W, torch.zeros(0, dtype=torch.int32, device="cuda"),
+                                e(0, sc.out_dim), e(0, 16, 16), need_dB=False, need_A=False)
+    torch.cuda.synchronize()
+    assert torch.count_nonzero(Wb) == 0
+    # an out-of-range element: NaN rows and SYMCON_EELEMENT, like the forward
+    ne3 = ne.clone()
+    ne3[33] = 6
+    dBb, Ab, _ = sc.backward2_raw(A, W, ne3, dB, uA)
+    torch.cuda.synchronize()
+    s, bad = sc.check_device_error()
+    assert s == _lib.SYMCON_EELEMENT and bad == 33
+    assert torch.isnan(dBb[33]).all() and torch.isnan(Ab[33]).all()
+    ok = torch.ones(129, dtype=torch.bool, device="cuda")
+    ok[33] = False
+    assert torch.isfinite(dBb[ok]).all() and torch.isfinite(Ab[ok]).all()
+
+
+def test_double_backward_autograd_force_loss():
+    """Training on forces: E = <R, B(A, W)>, F-like term dA = dE/dA with create_graph=True, loss
+    <V, dA> + <VW, dW>; its gradients against the oracle (uA terms: backward2; uW terms: the
+    forward and the dA backward with W -> VW, ops._SymconBwdFn)."""
+    from oracle.contraction import Problem, backward, backward2, forward
+    sc = _sc(3, 3, (0, 1), 4, 16)
+    A0, W0, ne, R0 = _inputs(sc, 90)
+    V = _uA(sc, 90, 0)
+    VW = torch.randn(W0.shape, generator=torch.Generator("cuda").manual_seed(3), device="cuda")
+    A, W, R = (x.clone().requires_grad_(True) for x in (A0, W0, R0))
+    E = (sc(A, W, ne) * R).sum()
+    dA, dW = torch.autograd.grad(E, (A, W), create_graph=True)
+    loss = (dA * V).sum() + (dW * VW).sum()
+    loss.backward()
+    prob = Problem(3, 3, (0, 1))
+    hA, hW, hne, hR, hV, hVW = _host(A0, W0, ne, R0, V, VW)
+    dBb, Ab, Wb = backward2(prob, hA, hW, hne, hR, hV)
+    Ab = Ab + backward(prob, hA, hVW, hne, hR)[0]
+    dBb = dBb + forward(prob, hA, hVW, hne)
+    assert _rel(A.grad.cpu(), Ab) < TOL
+    assert _rel(W.grad.cpu(), Wb) < TOL
+    assert _rel(R.grad.cpu(), dBb) < TOL
