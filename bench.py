@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--no-overlap", action="store_true", help="all-reduce dW after dA instead of overlapping")
     ap.add_argument("--sequential-bwd", action="store_true", help="run the dW and dA kernels back to back on one stream")
     ap.add_argument("--concurrent-bwd", action="store_true", help="run dA on a side stream concurrent with dW (default at N=1)")
+    ap.add_argument("--double-backward", action="store_true",
+                    help="force-training step (SURVEY §8(f) row 1): fwd + bwd + the double backward "
+                         "(dB_bar, A_bar, W_bar of <uA, dA>) per step; metric symcon_fwd_bwd_bwd2_nodes_per_s")
     return ap.parse_args()
 
 
@@ -94,7 +97,15 @@ def alg_ops(sc):
     dW = products + n_fold
     dA = len(prefixes3) + n_fold + 2 * deg3 + 2 * len(prefixes) + deg1
     path = fwd + (products + n_fold) + (n_fold + 2 * deg3 + 2 * len(prefixes) + deg1)
-    return {"fwd": fwd, "dA": dA, "dW": dW, "path": path, "n_fold": n_fold, "products": products,
+    # double backward (codegen symcon_bwd2 / symcon_bwd2_dW): per prefix p' (2 ops), p for degree-3
+    # groups (1); per degree-3 monomial mono' (2) and, in the tile kernel, A_bar_c, h, h' (3); per
+    # row one FMA into dB_bar (+ one into g for degree >= 2); per prefix group 2 (4 with h') FMAs
+    # into A_bar_a, A_bar_b. W_bar: products as above + one FMA per row.
+    rows1 = sum(1 for r in rows if deg[r[2]] == 1)
+    p3 = len(prefixes3)
+    bwd2 = rows1 + 2 * (n_fold - rows1) + 2 * len(prefixes) + p3 + 5 * deg3 + 4 * p3 + 2 * (len(prefixes) - p3)
+    bwd2_dW = n_fold + 2 * len(prefixes) + p3 + 2 * deg3
+    return {"fwd": fwd, "dA": dA, "dW": dW, "path": path, "bwd2": bwd2, "bwd2_dW": bwd2_dW, "n_fold": n_fold, "products": products,
             "prefixes": len(prefixes), "deg3_monomials": deg3, "n_sym": int(len(L))}
 
 
@@ -253,6 +264,7 @@ def run_ours(args):
     n_bins = shards.n_bins
     # pool of distinct bins for this rank (cycled): steps 0..POOL-1 of the epoch
     pool = []
+    uA = {}
     for q in range(POOL):
         step_id = q % shards.n_steps
         b = shards.bin_of(step_id)
@@ -263,6 +275,8 @@ def run_ours(args):
         B = torch.empty((N, sc.out_dim), device=dev)
         dA = torch.empty_like(A)
         pool.append((b, N, A, ne, dB, B, dA))
+        if args.double_backward:
+            uA[q] = gen_A(N, cfg.channels, sc.n_lm, dev, seed=100 * q + rank + 7)
     imbalance = max(shards.step_imbalance(q % shards.n_steps) for q in range(POOL))
     W = gen_W(cfg.n_elements, sc.block_sizes(), cfg.channels, dev)
     if world > 1:
@@ -273,10 +287,17 @@ def run_ours(args):
     conc = False if args.sequential_bwd else (True if args.concurrent_bwd else None)
     dp = DataParallelContraction(sc, overlap=not args.no_overlap, concurrent_bwd=conc)
 
+    def bwd2(q, A, ne, dB, counter):
+        # double backward of the same step (force loss): uA terms through symcon_backward2
+        sc.backward2_raw(A, W, ne, dB, uA[q % POOL], reuse=True)
+        counter.launches += sc.last_launch_count()
+
     def step(q):
         b, N, A, ne, dB, B, dA = pool[q % POOL]
         dp.forward(A, W, ne, B=B)
         dp.backward(A, W, ne, dB, dA=dA, dW=dW)
+        if args.double_backward:
+            bwd2(q, A, ne, dB, dp)
         return N
 
     for q in range(args.warmup):
@@ -312,6 +333,8 @@ def run_ours(args):
         b_, N_, A_, ne_, dB_, B_, dA_ = pool[q % POOL]
         seq.forward(A_, W, ne_, B=B_)
         seq.backward(A_, W, ne_, dB_, dA=dA_, dW=dW)
+        if args.double_backward:
+            bwd2(q, A_, ne_, dB_, seq)
     torch.cuda.synchronize()
     prof = _lib.symcon_profile_read(sc.plan)
     _lib.symcon_profile_enable(sc.plan, 0)
@@ -329,6 +352,8 @@ def run_ours(args):
     b, N, A, ne, dB, B, dA = pool[0]
     hA, hne, hdB = A.cpu().pin_memory(), ne.cpu().pin_memory(), dB.cpu().pin_memory()
     hdW = torch.empty(W.shape, dtype=W.dtype).pin_memory()
+    hU = uA[0].cpu().pin_memory() if args.double_backward else None
+    U2 = torch.empty_like(A) if args.double_backward else None
     dA2, dB2, ne2 = torch.empty_like(A), torch.empty_like(dB), torch.empty_like(ne)
     A2 = torch.empty_like(A)
 
@@ -339,6 +364,10 @@ def run_ours(args):
         Bx = dp.forward(A2, W, ne2, B=B)
         dp.backward(A2, W, ne2, dB2, dA=dA2, dW=dW)
         hdW.copy_(dW, non_blocking=True)
+        if args.double_backward:
+            U2.copy_(hU, non_blocking=True)
+            _, _, Wb = sc.backward2_raw(A2, W, ne2, dB2, U2, reuse=True)
+            hdW.copy_(Wb, non_blocking=True)
         return Bx
 
     e2e_steps = max(3, min(args.steps, 10))
@@ -358,8 +387,8 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(t2, op=dist.ReduceOp.MAX)
     e2e_value = N * world / (float(t2[0]) / 1e3)
-    h2d = hA.numel() * 4 + hne.numel() * 4 + hdB.numel() * 4
-    d2h = hdW.numel() * 4
+    h2d = hA.numel() * 4 + hne.numel() * 4 + hdB.numel() * 4 + (hU.numel() * 4 if hU is not None else 0)
+    d2h = hdW.numel() * 4 * (2 if args.double_backward else 1)
 
     if rank == 0:
         ops = alg_ops(sc)
@@ -371,7 +400,8 @@ def run_ours(args):
         if kern:
             cnt, tot_ms = prof[kern]
             avg_ms = tot_ms / max(cnt, 1)
-            per_nc = {"symcon_fwd": ops["fwd"], "symcon_bwd_dA": ops["dA"], "symcon_bwd_dW": ops["dW"]}.get(kern)
+            per_nc = {"symcon_fwd": ops["fwd"], "symcon_bwd_dA": ops["dA"], "symcon_bwd_dW": ops["dW"],
+                      "symcon_bwd2": ops["bwd2"], "symcon_bwd2_dW": ops["bwd2_dW"]}.get(kern)
             mean_nodes = nodes / args.steps
             if per_nc:
                 achieved = per_nc * mean_nodes * K / (avg_ms / 1e3) / 1e12  # T lane-ops/s
@@ -380,7 +410,8 @@ def run_ours(args):
                 nlm = (cfg.lmax_in + 1) ** 2
                 outc = sc.out_dim // K
                 alg_b = {"symcon_fwd": 4 * (nlm + outc), "symcon_bwd_dA": 4 * (2 * nlm + outc),
-                         "symcon_bwd_dW": 4 * (nlm + outc)}[kern] * mean_nodes * K
+                         "symcon_bwd_dW": 4 * (nlm + outc), "symcon_bwd2": 4 * (4 * nlm + 2 * outc),
+                         "symcon_bwd2_dW": 4 * (2 * nlm + outc)}[kern] * mean_nodes * K
                 traffic, tsrc = None, None
                 tpath = os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")
                 if os.path.exists(tpath) and args.config == "mp_medium":
@@ -394,13 +425,13 @@ def run_ours(args):
                         "algorithmic_bytes": alg_b, "avg_launch_ms": avg_ms,
                         "ops_per_node_channel": per_nc,
                         "peak_derivation": "148 SMs x 128 FP32 lanes x 1965 MHz (clocks.max.sm); FFMA probe measured 36.0 T/s"}
-        path_ops = ops["path"] * (nodes / args.steps) * K
+        path_ops = (ops["path"] + (ops["bwd2"] + ops["bwd2_dW"] if args.double_backward else 0)) * (nodes / args.steps) * K
         kernels = {k: {"launches": v[0], "avg_ms": v[1] / max(v[0], 1)} for k, v in prof.items()}
         out = {
-            "metric": "symcon_fwd_bwd_nodes_per_s", "value": value, "unit": "nodes/s", "n_gpus": world,
+            "metric": "symcon_fwd_bwd_bwd2_nodes_per_s" if args.double_backward else "symcon_fwd_bwd_nodes_per_s", "value": value, "unit": "nodes/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.config}_dp_step", "model": "MACE symmetric contraction",
+            "config": {"workload": f"{args.config}_dp_step" + ("_double_backward" if args.double_backward else ""), "model": "MACE symmetric contraction",
                        "channels": K, "out": "+".join(f"{K}x{L}{'e' if L % 2 == 0 else 'o'}" for L in cfg.out_L),
                        "lmax_in": cfg.lmax_in, "correlation": cfg.correlation, "elements": cfg.n_elements,
                        "capacity_nodes": CAPACITY, "bins": n_bins, "global_batch": int(nodes_all / args.steps),

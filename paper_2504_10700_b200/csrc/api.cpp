@@ -34,7 +34,7 @@ struct symcon_plan {
   int device = -1;
   int npad = 0;
   size_t unfold_smem = 0, tile_smem = 0, dw_smem = 0, dw2_smem = 0;
-  int dw_gpc = 1, dw_nz = 1;
+  int dw_gpc = 1, dw_nz = 1, dw2_gpc = 1, dw2_nz = 1;
   int grid_fwd = 0, grid_dA = 0, grid_bwd2 = 0;
   std::string source;
   cudaLibrary_t lib = nullptr;
@@ -301,6 +301,13 @@ static symcon_status build_common(int lmax_in, int corr, const int* out_L, int n
   // 52 rows x 8 warps, fewer smem reads per FMA), smaller groups for the 9-output large shape
   if (p->kc.dw_rows_per_group <= 0) p->kc.dw_rows_per_group = p->t.out_per_ch > 4 ? 26 : 52;
   if (p->kc.dw_groups_per_cta <= 0) p->kc.dw_groups_per_cta = p->t.out_per_ch > 4 ? 16 : 8;
+  // W_bar also holds the JVP direction rows in registers: at most 8 warps (255 registers each)
+  // (and enough warps that the register staging of A, U and dB stays small)
+  if (p->kc.dw2_rows_per_group <= 0) {
+    const int nrows = (int)p->t.rows.size();
+    p->kc.dw2_rows_per_group = p->t.out_per_ch > 4 ? 40 : std::min(52, std::max(16, (nrows + 7) / 8));
+  }
+  if (p->kc.dw2_groups_per_cta <= 0) p->kc.dw2_groups_per_cta = 8;
   p->source = generate_source(p->t, p->kc);
   *out = p;
   return SYMCON_OK;
@@ -366,6 +373,9 @@ symcon_status symcon_build_tables(int lmax_in, int correlation, const int* out_L
       const int ng = (nrows + p->kc.dw_rows_per_group - 1) / p->kc.dw_rows_per_group;  // must match codegen
       p->dw_nz = (ng + p->kc.dw_groups_per_cta - 1) / p->kc.dw_groups_per_cta;
       p->dw_gpc = (ng + p->dw_nz - 1) / p->dw_nz;
+      const int ng2 = (nrows + p->kc.dw2_rows_per_group - 1) / p->kc.dw2_rows_per_group;
+      p->dw2_nz = (ng2 + p->kc.dw2_groups_per_cta - 1) / p->kc.dw2_groups_per_cta;
+      p->dw2_gpc = (ng2 + p->dw2_nz - 1) / p->dw2_nz;
       p->dw_smem = sizeof(float) * (size_t)p->kc.dw_block_nodes * (p->t.n_lm + nout) * 34;
       if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_dW, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                            (int)p->dw_smem, device), "dW smem attribute");
@@ -681,8 +691,8 @@ symcon_status symcon_backward2(const symcon_plan* p, int64_t N, const float* A, 
   if (W_bar) {
     {
       Timed tm(p, K_BWD2_DW, st);
-      s = cuda_err(cudaLaunchKernel((const void*)p->k_bwd2_dW, dim3((unsigned)(w.max_items * p->dw_nz), (p->t.K + 31) / 32, 1),
-                                    dim3(32 * p->dw_gpc), args, p->dw2_smem, st), "launch symcon_bwd2_dW");
+      s = cuda_err(cudaLaunchKernel((const void*)p->k_bwd2_dW, dim3((unsigned)(w.max_items * p->dw2_nz), (p->t.K + 31) / 32, 1),
+                                    dim3(32 * p->dw2_gpc), args, p->dw2_smem, st), "launch symcon_bwd2_dW");
     }
     if (s) return s;
     Timed tm(p, K_UNFOLD, st);

@@ -64,6 +64,8 @@ struct KernelConfig {
   int dw_min_blocks = 2;           // __launch_bounds__ min blocks of the dW kernel
   int dw_rows_per_group = 0;       // transposed dW: rows j per warp (register accumulators); 0 = auto
   int dw_groups_per_cta = 0;       // transposed dW: warps per CTA; 0 = auto
+  int dw2_rows_per_group = 0;      // double-backward W_bar kernel (same layout): rows per warp; 0 = auto
+  int dw2_groups_per_cta = 0;      // double-backward W_bar kernel: warps per CTA; 0 = auto
   int dw_np_unroll = 1;            // transposed dW: unroll of the node-pair loop (software pipelining)
   int dw_batch = 1;                // transposed dW: rows whose products are emitted before their FMAs
   int dw_block_nodes = 8;          // transposed dW: nodes per smem stage
