@@ -16,6 +16,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="mp_medium")
     ap.add_argument("--iters", type=int, default=50)
+    ap.add_argument("--bwd2", action="store_true", help="also run the double backward each iteration")
     ap.add_argument("variants", nargs="*", default=[""])
     args = ap.parse_args()
     import torch
@@ -34,6 +35,8 @@ def main():
         if base is None:
             base = make_config_inputs(cfg, sc.block_sizes(), sc.out_dim, device="cuda")
         A, W, ne, dB = base
+        uA = torch.randn(A.shape, device="cuda", generator=torch.Generator("cuda").manual_seed(5)) if args.bwd2 else None
+        ck2 = None
         B = torch.empty((A.shape[0], sc.out_dim), device="cuda")
         dA, dW = torch.empty_like(A), torch.empty_like(W)
         for _ in range(3):
@@ -51,6 +54,8 @@ def main():
             for _ in range(args.iters):
                 sc.forward_raw(A, W, ne, B=B)
                 sc.backward_raw(A, W, ne, dB, dA=dA, dW=dW, reuse=True)
+                if args.bwd2:
+                    ck2 = sc.backward2_raw(A, W, ne, dB, uA, reuse=True)
             e1.record()
             torch.cuda.synchronize()
             clk.end()
@@ -59,7 +64,8 @@ def main():
         s, bad = sc.check_device_error()
         out = {"variant": v, "ms_per_step": e0.elapsed_time(e1) / args.iters, "status": s, "clocks": clk.summary(),
                "kernels_ms": {k: round(t / max(n, 1), 4) for k, (n, t) in prof.items()},
-               "checksum": [float(B.double().abs().sum()), float(dA.double().abs().sum()), float(dW.double().abs().sum())]}
+               "checksum": [float(B.double().abs().sum()), float(dA.double().abs().sum()), float(dW.double().abs().sum())]
+               + ([float(x.double().abs().sum()) for x in ck2] if ck2 else [])}
         print(json.dumps(out), flush=True)
         del sc
 
