@@ -287,10 +287,10 @@ def run_ours(args):
     conc = False if args.sequential_bwd else (True if args.concurrent_bwd else None)
     dp = DataParallelContraction(sc, overlap=not args.no_overlap, concurrent_bwd=conc)
 
-    def bwd2(q, A, ne, dB, counter):
-        # double backward of the same step (force loss): uA terms through symcon_backward2
-        sc.backward2_raw(A, W, ne, dB, uA[q % POOL], reuse=True)
-        counter.launches += sc.last_launch_count()
+    def bwd2(q, A, ne, dB, runner):
+        # double backward of the same step (force loss): uA terms through symcon_backward2, W_bar
+        # all-reduced over ranks like dW
+        runner.backward2(A, W, ne, dB, uA[q % POOL])
 
     def step(q):
         b, N, A, ne, dB, B, dA = pool[q % POOL]
@@ -366,7 +366,7 @@ def run_ours(args):
         hdW.copy_(dW, non_blocking=True)
         if args.double_backward:
             U2.copy_(hU, non_blocking=True)
-            _, _, Wb = sc.backward2_raw(A2, W, ne2, dB2, U2, reuse=True)
+            _, _, Wb = dp.backward2(A2, W, ne2, dB2, U2)
             hdW.copy_(Wb, non_blocking=True)
         return Bx
 

@@ -6,7 +6,8 @@
   PAPER.md:477), so no plan broadcast is needed.
 * DataParallelContraction: one training step of the contraction on this rank's bin: forward,
   backward dW, NCCL all-reduce of dW (the one cross-GPU exchange; PAPER.md:960 DDP all-reduce)
-  on a communication stream, overlapped with the backward dA kernel.
+  on a communication stream, overlapped with the backward dA kernel. For force training the
+  double backward's W_bar is all-reduced the same way, overlapped with its tile kernel.
 """
 import numpy as np
 import torch
@@ -110,3 +111,25 @@ class DataParallelContraction:
             self.launches += sc.last_launch_count()
         main.wait_stream(self.comm)
         return dA, dW
+
+    def backward2(self, A, W, node_elem, dB, uA, need_dB=True, need_A=True):
+        """Double backward of this rank's bin (force loss): W_bar first (all-reduced over ranks on
+        the communication stream), then dB_bar / A_bar, which stay local to the rank's nodes."""
+        sc = self.sc
+        if self.world == 1:
+            out = sc.backward2_raw(A, W, node_elem, dB, uA, need_dB, need_A, True, reuse=True)
+            self.launches += sc.last_launch_count()
+            return out
+        main = torch.cuda.current_stream(sc.device)
+        _, _, Wb = sc.backward2_raw(A, W, node_elem, dB, uA, False, False, True, reuse=True)
+        self.launches += sc.last_launch_count()
+        self.comm.wait_stream(main)
+        with torch.cuda.stream(self.comm):
+            dist.all_reduce(Wb, group=self.group)
+        Wb.record_stream(self.comm)
+        dBb = Ab = None
+        if need_dB or need_A:
+            dBb, Ab, _ = sc.backward2_raw(A, W, node_elem, dB, uA, need_dB, need_A, False, reuse=True)
+            self.launches += sc.last_launch_count()
+        main.wait_stream(self.comm)
+        return dBb, Ab, Wb

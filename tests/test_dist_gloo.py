@@ -55,13 +55,20 @@ def _worker(rank, world, port, out):
         mine.extend(int(g) for g in gids)
         A, dB, ne = _graph_inputs(gids, sizes, K, prob.n_paths, E)
         _, dW = oc.backward(A, W, ne, dB, want_dA=False) if len(ne) else (None, np.zeros(W.shape))
+        # double backward (force loss): W_bar is a W gradient too and is all-reduced the same way
+        uA = np.cos(A) if len(ne) else A
+        Wb = oc.backward2(A, W, ne, dB, uA, want_dB=False, want_A=False)[2] if len(ne) else np.zeros(W.shape)
         t = torch.from_numpy(dW.astype(np.float64))
+        tb = torch.from_numpy(Wb.astype(np.float64))
         dist.all_reduce(t)                                   # SUM over ranks (the NCCL call on GPU)
+        dist.all_reduce(tb)
         if rank == 0:
             gall = np.concatenate([sh.graphs(step, r) for r in range(world)])
             A2, dB2, ne2 = _graph_inputs(gall, sizes, K, prob.n_paths, E)
             _, ref = oc.backward(A2, W, ne2, dB2, want_dA=False)
             out.put(("step", step, float(np.abs(t.numpy() - ref).max()), float(np.abs(ref).max())))
+            refb = oc.backward2(A2, W, ne2, dB2, np.cos(A2), want_dB=False, want_A=False)[2]
+            out.put(("step", step, float(np.abs(tb.numpy() - refb).max()), float(np.abs(refb).max())))
     lst = [None] * world
     dist.all_gather_object(lst, mine)
     if rank == 0:

@@ -14,6 +14,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="mp_medium")
     ap.add_argument("--iters", type=int, default=3)
+    ap.add_argument("--bwd2", action="store_true", help="also run the double backward")
     args = ap.parse_args()
     import torch
     from paper_2504_10700_b200.ops import SymmetricContraction
@@ -24,6 +25,8 @@ def main():
     for _ in range(args.iters):
         B = sc.forward_raw(A, W, ne)
         dA, dW = sc.backward_raw(A, W, ne, dB)
+        if args.bwd2:
+            sc.backward2_raw(A, W, ne, dB, A, reuse=True)
     torch.cuda.synchronize()
     s, bad = sc.check_device_error()
     assert s == 0, (s, bad)
