@@ -396,3 +396,40 @@ def test_double_backward_autograd_force_loss():
     assert _rel(A.grad.cpu(), Ab) < TOL
     assert _rel(W.grad.cpu(), Wb) < TOL
     assert _rel(R.grad.cpu(), dBb) < TOL
+
+
+@pytest.mark.parametrize("config", ["mp_medium", "large"])
+def test_backward2_full_size_sampled(config):
+    """Double backward at full size: sampled nodes vs the oracle for dB_bar and A_bar (each
+    depends on its own node only); W_bar exactly on the three smallest elements (all their
+    nodes) and, over all elements, the bilinear identity <W, W_bar> = <dB, dB_bar>."""
+    from oracle.contraction import Problem
+    from oracle.ceval import OracleC
+    from synth.inputs import CONFIGS
+    cfg = CONFIGS[config]
+    n = cfg.n_nodes if config == "mp_medium" else 60000
+    sc = _sc(3, 3, cfg.out_L, cfg.n_elements, cfg.channels)
+    A, W, ne, dB = _inputs(sc, n, cfg.elem_dist, seed=1)
+    uA = _uA(sc, n, 1)
+    dBb, Ab, Wb = sc.backward2_raw(A, W, ne, dB, uA)
+    torch.cuda.synchronize()
+    assert sc.check_device_error()[0] == 0
+    oc = OracleC(Problem(3, 3, cfg.out_L))
+    rng = np.random.default_rng(7)
+    idx = torch.tensor(np.sort(rng.choice(n, 48, replace=False)), device="cuda")
+    ref = oc.backward2(*_host(A[idx], W, ne[idx], dB[idx], uA[idx]), want_W=False)
+    assert _rel(dBb[idx].cpu(), ref[0]) < TOL
+    assert _rel(Ab[idx].cpu(), ref[1]) < TOL
+    counts = torch.bincount(ne.long(), minlength=cfg.n_elements).cpu().numpy()
+    for z in np.argsort(counts)[:3]:
+        sel = torch.nonzero(ne == int(z)).flatten()
+        if sel.numel() == 0:
+            assert torch.count_nonzero(Wb[z]) == 0
+            continue
+        _, _, Wref = oc.backward2(*_host(A[sel], W, ne[sel], dB[sel], uA[sel]), want_dB=False, want_A=False)
+        assert _rel(Wb[z].cpu(), Wref[z]) < TOL
+    lhs = (W.double() * Wb.double()).sum().item()
+    rhs = (dB.double() * dBb.double()).sum().item()
+    assert abs(lhs - rhs) <= 1e-5 * (W.double().abs() * Wb.double().abs()).sum().item()
+    del A, dB, uA, dBb, Ab
+    torch.cuda.empty_cache()
