@@ -40,7 +40,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="mp_medium", choices=["off_small", "mp_medium", "large"])
-    ap.add_argument("--cpu-sample", type=int, default=4096, help="nodes in the oracle's bounded sample")
+    ap.add_argument("--cpu-sample", type=int, default=32768, help="nodes in the oracle's bounded sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-overlap", action="store_true", help="all-reduce dW after dA instead of overlapping")
     ap.add_argument("--sequential-bwd", action="store_true", help="run the dW and dA kernels back to back on one stream")
