@@ -20,8 +20,10 @@ Modules:
   packing      Alg. 1 Create-Balanced-Batches and the Eq. (1)-(5) metrics.
   ceval        ctypes wrapper around oracle/csrc/oracle_eval.c, a plain C
                fp64 OpenMP loop over the same raw tuples (timing + big parity).
+  tp           channelwise tensor product (Alg. 2) + edge->node
+               sum pooling (Eq. (1)); forward, backward (dY, dh, dR), brute force.
 
-Parity-unpinned functions: none in so3/paths/contraction/packing (see
+Parity-unpinned functions: none in so3/paths/contraction/packing/tp (see
 tests/test_oracle_*.py for each pin). Agreement with MACE/e3nn numeric tables
 is unpinned (no e3nn or MACE weights in this environment).
 """
