@@ -179,6 +179,51 @@ symcon_status symcon_pack_balanced(const int64_t* sizes, int64_t n, int64_t capa
                                    int32_t workers, int64_t* bin_offsets, int64_t* graph_ids,
                                    int64_t max_bins, int64_t* n_bins);
 
+/* ---- channelwise tensor product + edge->node sum ----------------
+ * Alg. 2 of the paper, the message construction that feeds the contraction,
+ * with the neighbour sum of Eq. (1):
+ *
+ *   A[i,k,l3 m3] = sum_{e: receiver[e] = i} sum_{paths p = (l1,l2,l3)} R[e,k,p]
+ *                  sum_{m1,m2} C^{l3 m3}_{l1 m1, l2 m2} Y[e, l1 m1] h[sender[e], k, l2 m2]
+ *
+ * C is the real coupling of symcon_real_cg. Paths: every (l1 <= lmax_y, l2 in hidden_l,
+ * l3 <= lmax_out) with |l1-l2| <= l3 <= l1+l2 and l1+l2+l3 even, ordered by (l1, l2, l3)
+ * (symcon_tp_path). Layouts (fp32, row-major, 16-byte aligned):
+ *   Y [E][(lmax_y+1)^2]  (lm = l^2+l+m)       h  [N][K][n_h] (hidden blocks in hidden_l order)
+ *   R [E][K][n_paths]                          A  [N][K][(lmax_out+1)^2] (the contraction's A)
+ *   sender, receiver: int32 [E]; receiver must be non-decreasing (edges sorted by receiver);
+ *   a violation or an index outside [0, N) is reported by symcon_tp_check_device_error
+ *   (SYMCON_EINVAL) and the outputs are unspecified. Nodes without incoming edges get A = 0.
+ * The backward returns the derivatives of <dA, A>: dY [E][n_y], dh [N][K][n_h] and
+ * dR [E][K][n_paths] (each overwritten; any may be NULL). Deterministic: fixed summation
+ * order, no floating-point atomics. */
+typedef struct symcon_tp_plan symcon_tp_plan; /* opaque */
+
+/* hidden_l: n_hidden strictly increasing irrep orders in [0,3]; lmax_y, lmax_out in [0,3];
+ * channels K >= 1. device < 0: host-only plan (tables and source, no kernels). */
+symcon_status symcon_tp_build(int lmax_y, const int* hidden_l, int n_hidden, int lmax_out, int channels,
+                              int device, symcon_tp_plan** plan);
+/* n_paths, n_y = (lmax_y+1)^2, n_h, n_out = (lmax_out+1)^2 */
+symcon_status symcon_tp_info(const symcon_tp_plan* plan, int32_t* n_paths, int32_t* n_y, int32_t* n_h,
+                             int32_t* n_out);
+symcon_status symcon_tp_path(const symcon_tp_plan* plan, int32_t p, int32_t* l1, int32_t* l2, int32_t* l3);
+size_t symcon_tp_workspace_bytes(const symcon_tp_plan* plan, int64_t num_nodes, int64_t num_edges);
+symcon_status symcon_tp_forward(const symcon_tp_plan* plan, int64_t num_nodes, int64_t num_edges,
+                                const float* Y, const float* h, const float* R, const int32_t* sender,
+                                const int32_t* receiver, float* A, void* ws, size_t ws_bytes,
+                                void* stream /* cudaStream_t */);
+symcon_status symcon_tp_backward(const symcon_tp_plan* plan, int64_t num_nodes, int64_t num_edges,
+                                 const float* Y, const float* h, const float* R, const int32_t* sender,
+                                 const int32_t* receiver, const float* dA, float* dY, float* dh, float* dR,
+                                 void* ws, size_t ws_bytes, void* stream /* cudaStream_t */);
+/* Synchronises `stream`; SYMCON_EINVAL if the last TP call on `ws` saw unsorted receivers or an
+ * out-of-range node index (*first_bad_edge = the first such edge), SYMCON_ECUDA on CUDA errors. */
+symcon_status symcon_tp_check_device_error(const symcon_tp_plan* plan, void* ws, void* stream,
+                                           int64_t* first_bad_edge);
+int32_t symcon_tp_last_launch_count(const symcon_tp_plan* plan);
+size_t symcon_tp_source(const symcon_tp_plan* plan, char* buf, size_t len);
+void symcon_tp_destroy(symcon_tp_plan* plan);
+
 #ifdef __cplusplus
 }
 #endif

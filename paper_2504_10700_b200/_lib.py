@@ -23,7 +23,9 @@ EXPORTS = ["symcon_build_tables", "symcon_plan_info", "symcon_plan_path", "symco
            "symcon_workspace_bytes", "symcon_forward", "symcon_backward", "symcon_backward_ex", "symcon_backward2", "symcon_check_device_error",
            "symcon_last_launch_count", "symcon_destroy", "symcon_status_string", "symcon_last_error",
            "symcon_pack_balanced", "symcon_precompile", "symcon_plan_source", "symcon_profile_enable",
-           "symcon_profile_reset", "symcon_profile_read"]
+           "symcon_profile_reset", "symcon_profile_read", "symcon_tp_build", "symcon_tp_info", "symcon_tp_path",
+           "symcon_tp_workspace_bytes", "symcon_tp_forward", "symcon_tp_backward", "symcon_tp_check_device_error",
+           "symcon_tp_last_launch_count", "symcon_tp_source", "symcon_tp_destroy"]
 
 
 class SymconInfo(ctypes.Structure):
@@ -133,8 +135,8 @@ def symcon_real_cg(l1, l2, L):
 
 def symcon_plan_source(plan):
     n = lib.symcon_plan_source(plan, None, 0)
-    buf = ctypes.create_string_buffer(n)
-    lib.symcon_plan_source(plan, buf, n)
+    buf = ctypes.create_string_buffer(n + 1)
+    lib.symcon_plan_source(plan, buf, n + 1)
     return buf.value.decode()
 
 
@@ -212,3 +214,78 @@ def symcon_profile_read(plan):
     ms = (ctypes.c_double * PROFILE_MAX)()
     n = lib.symcon_profile_read(plan, names, counts, ms)
     return {names[i].decode(): (int(counts[i]), float(ms[i])) for i in range(n)}
+
+
+# ------------------------------------------------------------ channelwise TP (symcon_tp_*)
+lib.symcon_tp_build.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                ctypes.c_int, ctypes.POINTER(_vp)]
+lib.symcon_tp_info.argtypes = [_vp] + [ctypes.POINTER(_i32)] * 4
+lib.symcon_tp_path.argtypes = [_vp, _i32] + [ctypes.POINTER(_i32)] * 3
+lib.symcon_tp_workspace_bytes.argtypes = [_vp, _i64, _i64]
+lib.symcon_tp_workspace_bytes.restype = _sz
+lib.symcon_tp_forward.argtypes = [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
+lib.symcon_tp_backward.argtypes = [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
+lib.symcon_tp_check_device_error.argtypes = [_vp, _vp, _vp, ctypes.POINTER(_i64)]
+lib.symcon_tp_last_launch_count.argtypes = [_vp]
+lib.symcon_tp_last_launch_count.restype = _i32
+lib.symcon_tp_source.argtypes = [_vp, ctypes.c_char_p, _sz]
+lib.symcon_tp_source.restype = _sz
+lib.symcon_tp_destroy.argtypes = [_vp]
+lib.symcon_tp_destroy.restype = None
+for _n in ("symcon_tp_build", "symcon_tp_info", "symcon_tp_path", "symcon_tp_forward", "symcon_tp_backward",
+           "symcon_tp_check_device_error"):
+    getattr(lib, _n).restype = ctypes.c_int
+
+
+def symcon_tp_build(lmax_y, hidden_l, lmax_out, channels, device):
+    arr = (ctypes.c_int * len(hidden_l))(*hidden_l)
+    plan = _vp()
+    check(lib.symcon_tp_build(lmax_y, arr, len(hidden_l), lmax_out, channels, device, ctypes.byref(plan)),
+          "symcon_tp_build")
+    return plan
+
+
+def symcon_tp_info(plan):
+    v = [_i32() for _ in range(4)]
+    check(lib.symcon_tp_info(plan, *[ctypes.byref(x) for x in v]), "symcon_tp_info")
+    return tuple(x.value for x in v)   # n_paths, n_y, n_h, n_out
+
+
+def symcon_tp_path(plan, p):
+    v = [_i32() for _ in range(3)]
+    check(lib.symcon_tp_path(plan, p, *[ctypes.byref(x) for x in v]), "symcon_tp_path")
+    return tuple(x.value for x in v)
+
+
+def symcon_tp_workspace_bytes(plan, num_nodes, num_edges):
+    return lib.symcon_tp_workspace_bytes(plan, num_nodes, num_edges)
+
+
+def symcon_tp_forward(plan, N, E, Y, h, R, sender, receiver, A, ws, ws_bytes, stream):
+    check(lib.symcon_tp_forward(plan, N, E, Y, h, R, sender, receiver, A, ws, ws_bytes, stream), "symcon_tp_forward")
+
+
+def symcon_tp_backward(plan, N, E, Y, h, R, sender, receiver, dA, dY, dh, dR, ws, ws_bytes, stream):
+    check(lib.symcon_tp_backward(plan, N, E, Y, h, R, sender, receiver, dA, dY, dh, dR, ws, ws_bytes, stream),
+          "symcon_tp_backward")
+
+
+def symcon_tp_check_device_error(plan, ws, stream):
+    bad = _i64(-1)
+    s = lib.symcon_tp_check_device_error(plan, ws, stream, ctypes.byref(bad))
+    return s, bad.value
+
+
+def symcon_tp_source(plan):
+    n = lib.symcon_tp_source(plan, None, 0)
+    buf = ctypes.create_string_buffer(n + 1)
+    lib.symcon_tp_source(plan, buf, n + 1)
+    return buf.value.decode()
+
+
+def symcon_tp_destroy(plan):
+    lib.symcon_tp_destroy(plan)
+
+
+def symcon_tp_last_launch_count(plan):
+    return lib.symcon_tp_last_launch_count(plan)

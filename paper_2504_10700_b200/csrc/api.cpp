@@ -257,6 +257,11 @@ symcon_status validate_build(int lmax_in, int corr, const int* out_L, int n_out,
 
 }  // namespace
 
+namespace symcon {
+bool compile_cubin(const std::string& src, std::vector<char>& cubin) { return get_cubin(src, cubin, nullptr); }
+symcon_status cuda_status(cudaError_t e, const char* what) { return cuda_err(e, what); }
+}  // namespace symcon
+
 extern "C" {
 
 const char* symcon_status_string(symcon_status s) {

@@ -78,6 +78,9 @@ std::string generate_source(const Tables& t, const KernelConfig& kc);
 // apply "key=value,..." overrides (env SYMCON_KCONFIG) to a KernelConfig; returns false on bad keys
 bool parse_kernel_config(const char* spec, KernelConfig& kc);
 
+// ---- api.cpp helpers shared with tp.cpp
+bool compile_cubin(const std::string& src, std::vector<char>& cubin);  // NVRTC sm_100a + disk cache
+
 // ---- pack.cpp
 int64_t pack_balanced(const int64_t* sizes, int64_t n, int64_t C, int G,
                       std::vector<std::vector<int64_t>>& bins);

@@ -30,4 +30,20 @@ size_t bucket_chunks(int64_t N);
 // stot[z][j][k] = sum over items it of element z (item order) of spart[it][j][k]
 int reduce_items_launch(const float* spart, const int* item_off, int E, int npad, int K, float* stot, cudaStream_t st);
 
+// channelwise TP (tp_static.cu)
+struct TPCsrArgs {
+  const int* sender;
+  const int* receiver;
+  int N, E;
+  unsigned long long* err;  // first bad edge (~0 = none)
+  int* recv_off;            // [N+1]
+  int* send_cnt;            // [N]      (sender CSR; all NULL to skip)
+  int* send_off;            // [N+1]
+  int* send_cur;            // [N]
+  int* send_perm;           // [E]
+};
+int tp_csr_launch(const TPCsrArgs& a, cudaStream_t st);
+int tp_dh_reduce_launch(const float* dhe, const int* off, const int* perm, int N, int K, int nh, float* dh,
+                        cudaStream_t st);
+
 }  // namespace symcon

@@ -176,3 +176,91 @@ class _SymconBwdFn(torch.autograd.Function):
                 a, _ = sc.backward_raw(A, uW, node_elem, dB, need_dW=False)
                 A_bar = a if A_bar is None else A_bar.add_(a)
         return A_bar, W_bar, None, dB_bar, None
+
+
+class ChannelwiseTP:
+    """Alg. 2 channelwise tensor product + neighbour sum (symcon_tp_*).
+
+        tp = ChannelwiseTP(lmax_y=3, hidden_l=(0, 1), lmax_out=3, channels=128, device=0)
+        A = tp(Y, h, R, sender, receiver)     # A[N][K][(lmax_out+1)^2]; autograd gives dY, dh, dR
+
+    Edges must be sorted by receiver. All arithmetic runs in libsymcon's kernels."""
+
+    def __init__(self, lmax_y, hidden_l, lmax_out, channels, device=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("ChannelwiseTP needs a CUDA device (libsymcon has no CPU path)")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
+        self.channels = channels
+        with torch.cuda.device(self.device):
+            self.plan = _lib.symcon_tp_build(lmax_y, list(hidden_l), lmax_out, channels, self.device.index)
+        self.n_paths, self.n_y, self.n_h, self.n_out = _lib.symcon_tp_info(self.plan)
+        self._ws = None
+
+    def __del__(self):
+        plan = getattr(self, "plan", None)
+        if plan is not None:
+            _lib.symcon_tp_destroy(plan)
+            self.plan = None
+
+    def workspace(self, N, E):
+        nbytes = _lib.symcon_tp_workspace_bytes(self.plan, N, E)
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def _check(self, Y, h, R, sender, receiver):
+        N, E, K = h.shape[0], sender.shape[0], self.channels
+        for t in (Y, h, R):
+            assert t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()
+        assert Y.shape == (E, self.n_y) and h.shape == (N, K, self.n_h) and R.shape == (E, K, self.n_paths)
+        assert sender.dtype == torch.int32 and receiver.dtype == torch.int32 and receiver.shape == (E,)
+        return N, E
+
+    def forward_raw(self, Y, h, R, sender, receiver, A=None):
+        N, E = self._check(Y, h, R, sender, receiver)
+        if A is None:
+            A = torch.empty((N, self.channels, self.n_out), dtype=torch.float32, device=self.device)
+        ws = self.workspace(N, E)
+        ptr = lambda t: t.data_ptr() if t.numel() else None
+        _lib.symcon_tp_forward(self.plan, N, E, ptr(Y), ptr(h), ptr(R), ptr(sender), ptr(receiver), A.data_ptr(),
+                               ws.data_ptr(), ws.numel(), _stream_ptr(self.device))
+        return A
+
+    def backward_raw(self, Y, h, R, sender, receiver, dA, need_Y=True, need_h=True, need_R=True):
+        N, E = self._check(Y, h, R, sender, receiver)
+        assert dA.dtype == torch.float32 and dA.is_contiguous() and dA.shape == (N, self.channels, self.n_out)
+        dY = torch.empty_like(Y) if need_Y else None
+        dh = torch.empty_like(h) if need_h else None
+        dR = torch.empty_like(R) if need_R else None
+        ws = self.workspace(N, E)
+        ptr = lambda t: t.data_ptr() if (t is not None and t.numel()) else None
+        _lib.symcon_tp_backward(self.plan, N, E, ptr(Y), ptr(h), ptr(R), ptr(sender), ptr(receiver), dA.data_ptr(),
+                                ptr(dY), ptr(dh), ptr(dR), ws.data_ptr(), ws.numel(), _stream_ptr(self.device))
+        return dY, dh, dR
+
+    def check_device_error(self):
+        if self._ws is None:
+            return 0, -1
+        return _lib.symcon_tp_check_device_error(self.plan, self._ws.data_ptr(), _stream_ptr(self.device))
+
+    def last_launch_count(self):
+        return _lib.symcon_tp_last_launch_count(self.plan)
+
+    def __call__(self, Y, h, R, sender, receiver):
+        return _TPFn.apply(Y, h, R, sender, receiver, self)
+
+
+class _TPFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, Y, h, R, sender, receiver, tp):
+        ctx.tp = tp
+        Y, h, R = Y.contiguous(), h.contiguous(), R.contiguous()
+        ctx.save_for_backward(Y, h, R, sender, receiver)
+        return tp.forward_raw(Y, h, R, sender, receiver)
+
+    @staticmethod
+    @torch.autograd.function.once_differentiable
+    def backward(ctx, dA):
+        Y, h, R, sender, receiver = ctx.saved_tensors
+        dY, dh, dR = ctx.tp.backward_raw(Y, h, R, sender, receiver, dA.contiguous(), *ctx.needs_input_grad[:3])
+        return dY, dh, dR, None, None, None

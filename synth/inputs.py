@@ -155,3 +155,34 @@ def make_config_inputs(cfg, block_sizes, out_dim, device="cpu", seed=0, n_nodes=
     ne = gen_node_elem(N, cfg.n_elements, cfg.elem_dist, device, seed)
     dB = gen_dB(N, out_dim, device, seed)
     return A, W, ne, dB
+
+
+# ------------------------------------------------------------------ channelwise TP (§8(f) row 2)
+# Seeds: Y=6, h=7, R=8, graph=9 (each offset by `seed`). Degree: 30 incoming edges per node
+# (deg ~45.6 for liquid water, others unpinned -> 30), capped at n-1 inside
+# each molecule; senders uniform over the other nodes of the receiver's molecule.
+def gen_tp_graph(sizes, deg=30, seed=0):
+    """Receiver-sorted edge list (sender, receiver) int32 over molecules of the given sizes
+    laid out consecutively."""
+    rng = np.random.default_rng(9 + seed)
+    sizes = np.asarray(sizes, dtype=np.int64)
+    starts = np.concatenate([[0], np.cumsum(sizes)[:-1]])
+    node_mol_start = np.repeat(starts, sizes)
+    node_mol_size = np.repeat(sizes, sizes)
+    N = int(sizes.sum())
+    d = np.minimum(deg, node_mol_size - 1)
+    receiver = np.repeat(np.arange(N, dtype=np.int64), d)
+    # sender = another node of the same molecule: offset in [1, n-1] from the receiver, cyclic
+    n = np.repeat(node_mol_size, d)
+    off = 1 + (rng.random(receiver.shape[0]) * (n - 1)).astype(np.int64)
+    local = (receiver - np.repeat(node_mol_start, d) + off) % n
+    sender = np.repeat(node_mol_start, d) + local
+    return sender.astype(np.int32), receiver.astype(np.int32)
+
+
+def gen_tp_inputs(n_nodes, n_edges, channels, n_y, n_h, n_paths, device="cpu", seed=0):
+    gy, gh, gr = _gen(device, 6 + seed), _gen(device, 7 + seed), _gen(device, 8 + seed)
+    Y = torch.randn((n_edges, n_y), generator=gy, device=device, dtype=torch.float32)
+    h = torch.randn((n_nodes, channels, n_h), generator=gh, device=device, dtype=torch.float32)
+    R = torch.randn((n_edges, channels, n_paths), generator=gr, device=device, dtype=torch.float32)
+    return Y, h, R

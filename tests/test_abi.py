@@ -120,3 +120,26 @@ def test_pack_table2_speed_and_balance(L):
     assert len(offs) - 1 == 195144 and (len(offs) - 1) % 8 == 0
     assert loads.max() <= 3072 and np.sort(ids).tolist() == list(range(len(sizes)))
     assert dt < 2.65 * 1.5, dt     # 2.65M graphs: <= 1.5x the paper's per-graph rate
+
+
+@pytest.mark.parametrize("lmax_y,hidden,lmax_out", [(3, (0, 1), 3), (3, (0,), 3), (2, (0, 1, 2), 2), (1, (1,), 1),
+                                                    (3, (0, 1, 2, 3), 3)])
+def test_tp_plan_paths_match_oracle(L, lmax_y, hidden, lmax_out):
+    from oracle.tp import TPProblem
+    prob = TPProblem(lmax_y, hidden, lmax_out)
+    plan = L.symcon_tp_build(lmax_y, list(hidden), lmax_out, 8, -1)
+    n_paths, n_y, n_h, n_out = L.symcon_tp_info(plan)
+    assert (n_paths, n_y, n_h, n_out) == (prob.n_paths, prob.n_y, prob.n_h, prob.n_out)
+    assert [L.symcon_tp_path(plan, p) for p in range(n_paths)] == [prob.path_l(p) for p in range(n_paths)]
+    src = L.symcon_tp_source(plan)
+    assert "symcon_tp_fwd" in src and "symcon_tp_bwd" in src
+    with pytest.raises(L.SymconError):   # host-only plan cannot compute
+        L.symcon_tp_forward(plan, 4, 4, 16, 16, 16, 16, 16, 16, 16, 1 << 20, None)
+    L.symcon_tp_destroy(plan)
+
+
+def test_tp_invalid_arguments(L):
+    for args in [(4, [0], 3), (3, [1, 0], 3), (3, [], 3), (3, [0], 4), (0, [1], 0)]:
+        with pytest.raises(L.SymconError) as e:
+            L.symcon_tp_build(args[0], args[1], args[2], 8, -1)
+        assert e.value.status == L.SYMCON_EINVAL
