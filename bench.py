@@ -45,6 +45,10 @@ def parse():
     ap.add_argument("--no-overlap", action="store_true", help="all-reduce dW after dA instead of overlapping")
     ap.add_argument("--sequential-bwd", action="store_true", help="run the dW and dA kernels back to back on one stream")
     ap.add_argument("--concurrent-bwd", action="store_true", help="run dA on a side stream concurrent with dW (default at N=1)")
+    ap.add_argument("--channelwise-tp", action="store_true",
+                    help="SURVEY §8(f) row 2: channelwise tensor product (Alg. 2) + neighbour sum, forward + "
+                         "backward (dY, dh, dR) per step on the bin's molecular graphs (degree 30); "
+                         "metric symcon_tp_fwd_bwd_edges_per_s")
     ap.add_argument("--double-backward", action="store_true",
                     help="force-training step (SURVEY §8(f) row 1): fwd + bwd + the double backward "
                          "(dB_bar, A_bar, W_bar of <uA, dA>) per step; metric symcon_fwd_bwd_bwd2_nodes_per_s")
@@ -456,10 +460,206 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# ----------------------------------------------------------------------------- channelwise TP
+def tp_bytes(N, E, K, P, NH, NY, NOUT):
+    """Algorithmic HBM bytes of one TP step: every input read once, every output
+    written once (h, dA per node; R, Y per edge; no intermediate)."""
+    fwd = 4 * (E * K * P + N * K * NH + E * NY + N * K * NOUT) + 8 * E
+    bwd = 4 * (E * K * P + N * K * NH + E * NY + N * K * NOUT) + 8 * E + 4 * (E * NY + N * K * NH + E * K * P)
+    return fwd, bwd
+
+
+def run_tp(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2504_10700_b200.ops import ChannelwiseTP
+    from paper_2504_10700_b200.dist import BinPackedShards
+    from synth.inputs import table2_sizes, gen_tp_graph, gen_tp_inputs
+    K, LMAX_Y, HIDDEN, LMAX_OUT, DEG = 128, 3, (0, 1), 3, 30
+    tp = ChannelwiseTP(LMAX_Y, HIDDEN, LMAX_OUT, K, device=local)
+    sizes = table2_sizes(seed=0)
+    shards = BinPackedShards(sizes, CAPACITY, world, rank)
+    pool = []
+    for q in range(2):
+        b = shards.bin_of(q % shards.n_steps)
+        snd, rcv = gen_tp_graph(sizes[shards.graphs(q % shards.n_steps)], DEG, seed=b)
+        N, E = int(sizes[shards.graphs(q % shards.n_steps)].sum()), len(snd)
+        Y, h, R = gen_tp_inputs(N, E, K, tp.n_y, tp.n_h, tp.n_paths, dev, seed=100 * q + rank)
+        dA = torch.randn((N, K, tp.n_out), generator=torch.Generator(dev).manual_seed(q), device=dev)
+        pool.append(dict(N=N, E=E, Y=Y, h=h, R=R, s=torch.from_numpy(snd).to(dev), r=torch.from_numpy(rcv).to(dev),
+                         dA=dA, A=torch.empty((N, K, tp.n_out), device=dev), dY=torch.empty_like(Y),
+                         dh=torch.empty_like(h), dR=torch.empty_like(R)))
+    tp.workspace(max(x["N"] for x in pool), max(x["E"] for x in pool))
+    from paper_2504_10700_b200 import _lib
+    launches = [0]
+
+    def step(q, ev=None):
+        x = pool[q % len(pool)]
+        st = torch.cuda.current_stream(dev).cuda_stream
+        ws = tp._ws
+        if ev:
+            ev[0].record()
+        _lib.symcon_tp_forward(tp.plan, x["N"], x["E"], x["Y"].data_ptr(), x["h"].data_ptr(), x["R"].data_ptr(),
+                               x["s"].data_ptr(), x["r"].data_ptr(), x["A"].data_ptr(), ws.data_ptr(), ws.numel(), st)
+        launches[0] += tp.last_launch_count()
+        if ev:
+            ev[1].record()
+        _lib.symcon_tp_backward(tp.plan, x["N"], x["E"], x["Y"].data_ptr(), x["h"].data_ptr(), x["R"].data_ptr(),
+                                x["s"].data_ptr(), x["r"].data_ptr(), x["dA"].data_ptr(), x["dY"].data_ptr(),
+                                x["dh"].data_ptr(), x["dR"].data_ptr(), ws.data_ptr(), ws.numel(), st)
+        launches[0] += tp.last_launch_count()
+        if ev:
+            ev[2].record()
+        return x["N"], x["E"]
+
+    for q in range(args.warmup):
+        step(q)
+    torch.cuda.synchronize()
+    st_, bad = tp.check_device_error()
+    assert st_ == 0, (st_, bad)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches[0] = 0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nodes = edges = 0
+    with ClockSampler(local) as clk:
+        clk.start()
+        e0.record()
+        for q in range(args.steps):
+            n_, e_ = step(q)
+            nodes += n_
+            edges += e_
+        e1.record()
+        torch.cuda.synchronize()
+        clk.end()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    n_launch = launches[0]
+    # per-phase times (fwd, bwd) from a separate pass of the same steps
+    tf = tb = 0.0
+    for q in range(args.steps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        step(q, ev)
+        torch.cuda.synchronize()
+        tf += ev[0].elapsed_time(ev[1])
+        tb += ev[1].elapsed_time(ev[2])
+    t = torch.tensor([ms, nodes, edges], dtype=torch.float64, device=dev)
+    if world > 1:
+        tt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(tt, t)
+        ms_max = max(float(x[0]) for x in tt)
+        edges_all = sum(float(x[2]) for x in tt)
+        nodes_all = sum(float(x[1]) for x in tt)
+    else:
+        ms_max, edges_all, nodes_all = ms, float(edges), float(nodes)
+    value = edges_all / (ms_max / 1e3)
+    # e2e: host inputs (pinned) copied in, gradients copied out, every step
+    x = pool[0]
+    hY, hh, hR, hs, hr, hdA = (x[k].cpu().pin_memory() for k in ("Y", "h", "R", "s", "r", "dA"))
+    hdR = torch.empty(x["R"].shape).pin_memory()
+    hdh = torch.empty(x["h"].shape).pin_memory()
+    hdY = torch.empty(x["Y"].shape).pin_memory()
+    dev_bufs = {k: torch.empty_like(x[k]) for k in ("Y", "h", "R", "s", "r", "dA")}
+
+    def e2e():
+        for k, hsrc in zip(("Y", "h", "R", "s", "r", "dA"), (hY, hh, hR, hs, hr, hdA)):
+            dev_bufs[k].copy_(hsrc, non_blocking=True)
+        tp.forward_raw(dev_bufs["Y"], dev_bufs["h"], dev_bufs["R"], dev_bufs["s"], dev_bufs["r"], A=x["A"])
+        dY, dh, dR = tp.backward_raw(dev_bufs["Y"], dev_bufs["h"], dev_bufs["R"], dev_bufs["s"], dev_bufs["r"],
+                                     dev_bufs["dA"])
+        hdY.copy_(dY, non_blocking=True)
+        hdh.copy_(dh, non_blocking=True)
+        hdR.copy_(dR, non_blocking=True)
+
+    e2e()
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ne2e = 3
+    f0.record()
+    for _ in range(ne2e):
+        e2e()
+    f1.record()
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1) / ne2e
+    if rank == 0:
+        P, NH, NY, NOUT = tp.n_paths, tp.n_h, tp.n_y, tp.n_out
+        fb, bb = tp_bytes(x["N"], x["E"], K, P, NH, NY, NOUT)
+        mean_e = edges / args.steps
+        mean_n = nodes / args.steps
+        fb, bb = tp_bytes(mean_n, mean_e, K, P, NH, NY, NOUT)
+        peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+            os.path.join(ROOT, "MEASURED_PEAKS.json")) else 7700.0
+        avg_f, avg_b = tf / args.steps, tb / args.steps
+        dom = ("symcon_tp_bwd", bb, avg_b) if avg_b >= avg_f else ("symcon_tp_fwd", fb, avg_f)
+        achieved = dom[1] / (dom[2] / 1e3) / 1e9
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "r01", "ncu_tp_traffic.json")
+        if os.path.exists(tpath):
+            tj = json.load(open(tpath))
+            rec = tj.get("kernels", {}).get(dom[0])
+            if rec:
+                traffic = rec["dram_bytes_read"] + rec["dram_bytes_write"]
+        h2d = sum(t.numel() * t.element_size() for t in (hY, hh, hR, hs, hr, hdA))
+        d2h = sum(t.numel() * t.element_size() for t in (hdY, hdh, hdR))
+        cpu = None
+        if not args.no_cpu_baseline:
+            from oracle.tp import TPProblem, forward as tpf, backward as tpb
+            prob = TPProblem(LMAX_Y, HIDDEN, LMAX_OUT)
+            hs_np, hr_np = x["s"].cpu().numpy(), x["r"].cpu().numpy()
+            sel = np.nonzero(hr_np < 2000)[0]           # edges into the first 2000 nodes
+            te = torch.from_numpy(sel).to(dev)
+            cY, cR = x["Y"][te].cpu().numpy(), x["R"][te].cpu().numpy()
+            ch_, cdA = x["h"].cpu().numpy(), x["dA"].cpu().numpy()
+            t0 = time.time()
+            tpf(prob, cY, ch_, cR, hs_np[sel], hr_np[sel], x["N"])
+            tpb(prob, cY, ch_, cR, hs_np[sel], hr_np[sel], x["N"], cdA)
+            dt = time.time() - t0
+            cpu = {"value": len(sel) / dt, "unit": "edges/s", "cores": 1, "kind": "oracle",
+                   "sample": f"{len(sel)} edges (into the first 2000 nodes of one bin), fwd + bwd, numpy fp64 oracle "
+                             f"(oracle/tp.py), {dt:.1f} s"}
+        out = {
+            "metric": "symcon_tp_fwd_bwd_edges_per_s", "value": value, "unit": "edges/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "channelwise_tp_mp_layer2_dp_step", "channels": K, "lmax_y": LMAX_Y,
+                       "hidden": "+".join(f"{K}x{l}{'e' if l % 2 == 0 else 'o'}" for l in HIDDEN),
+                       "lmax_out": LMAX_OUT, "paths": P, "degree": DEG, "capacity_nodes": CAPACITY,
+                       "nodes_per_step": int(nodes_all / args.steps), "edges_per_step": int(edges_all / args.steps),
+                       "parallelism": f"dp{world}", "l2": "inputs > L2 (R 7.5 GB per bin), 2-bin pool"},
+            "nodes_per_s": nodes_all / (ms_max / 1e3),
+            "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "algorithmic_bytes": dom[1],
+                         "avg_launch_ms": dom[2],
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)",
+                         "note": "time of the launch group (CSR + kernel [+ dh reduce]) from CUDA events"},
+            "phases_ms": {"fwd": avg_f, "bwd": avg_b},
+            "clocks": clk.summary(), "gpu_launches": n_launch,
+            "e2e": {"value": x["E"] / (e2e_ms / 1e3), "unit": "edges/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "note": "pinned host Y, h, R, edges, dA in; dY, dh, dR out"},
+        }
+        if cpu:
+            out["cpu_baseline"] = cpu
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.channelwise_tp:
+        run_tp(args)
     else:
         run_ours(args)
 
