@@ -615,7 +615,7 @@ def run_tp(args):
             from oracle.tp import TPProblem, forward as tpf, backward as tpb
             prob = TPProblem(LMAX_Y, HIDDEN, LMAX_OUT)
             hs_np, hr_np = x["s"].cpu().numpy(), x["r"].cpu().numpy()
-            sel = np.nonzero(hr_np < 2000)[0]           # edges into the first 2000 nodes
+            sel = np.nonzero(hr_np < 800)[0]            # edges into the first 800 nodes
             te = torch.from_numpy(sel).to(dev)
             cY, cR = x["Y"][te].cpu().numpy(), x["R"][te].cpu().numpy()
             ch_, cdA = x["h"].cpu().numpy(), x["dA"].cpu().numpy()
@@ -624,7 +624,7 @@ def run_tp(args):
             tpb(prob, cY, ch_, cR, hs_np[sel], hr_np[sel], x["N"], cdA)
             dt = time.time() - t0
             cpu = {"value": len(sel) / dt, "unit": "edges/s", "cores": 1, "kind": "oracle",
-                   "sample": f"{len(sel)} edges (into the first 2000 nodes of one bin), fwd + bwd, numpy fp64 oracle "
+                   "sample": f"{len(sel)} edges (into the first 800 nodes of one bin), fwd + bwd, numpy fp64 oracle "
                              f"(oracle/tp.py), {dt:.1f} s"}
         out = {
             "metric": "symcon_tp_fwd_bwd_edges_per_s", "value": value, "unit": "edges/s", "n_gpus": world,

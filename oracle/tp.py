@@ -15,8 +15,8 @@ Readings (t1-t6):
       contraction, readings s7/s8); a path is one (l1, l2, l3) with the triangle rule and
       natural parity (l1 + l2 + l3 even: Y_l1 has parity (-1)^l1, h_l2 (-1)^l2, and the output
       irrep l3 of the A feature row has natural parity, like the contraction's input).
-  t2  paths ordered lexicographically by (l1, l2, l3); R has one weight per (edge, channel,
-      path) in that order: R[E][K][P].
+  t2  paths ordered lexicographically by (l1, l2, l3); R has one weight per (edge, path,
+      channel), channel fastest: R[E][P][K] (e3nn's per-instruction weight blocks).
   t3  h holds the hidden irreps `hidden_l` (strictly increasing l, one block of 2l+1
       components each) per (node, channel): h[N][K][n_h]; Y[E][(lmax_y+1)^2] with lm = l^2 + l + m.
   t4  output A[N][K][(lmax_out+1)^2] (the contraction's input layout); nodes without incoming
@@ -68,7 +68,7 @@ class TPProblem:
 def _check(prob, Y, h, R, sender, receiver, N):
     E = len(sender)
     K = h.shape[1]
-    assert Y.shape == (E, prob.n_y) and h.shape == (N, K, prob.n_h) and R.shape == (E, K, prob.n_paths)
+    assert Y.shape == (E, prob.n_y) and h.shape == (N, K, prob.n_h) and R.shape == (E, prob.n_paths, K)
     assert len(receiver) == E
     return E, K
 
@@ -78,12 +78,12 @@ def messages(prob, Y, h, R, sender):
     Y, h, R = (np.asarray(x, dtype=np.float64) for x in (Y, h, R))
     sender = np.asarray(sender, dtype=np.int64)
     hs_all = h[sender]                                    # h_{j,k,.} of each edge's sender
-    E, K = R.shape[:2]
+    E, K = R.shape[0], R.shape[2]
     M = np.zeros((E, K, prob.n_out))
     for p in range(prob.n_paths):
         ys, hs, As, C = prob.blocks(p)
-        # sum_{m1,m2} C[m3,m1,m2] Y[e,m1] h[e,k,m2], weighted by R[e,k,p]
-        M[:, :, As] += R[:, :, p, None] * np.einsum("cab,ea,ekb->ekc", C, Y[:, ys], hs_all[:, :, hs])
+        # sum_{m1,m2} C[m3,m1,m2] Y[e,m1] h[e,k,m2], weighted by R[e,p,k]
+        M[:, :, As] += R[:, p, :, None] * np.einsum("cab,ea,ekb->ekc", C, Y[:, ys], hs_all[:, :, hs])
     return M
 
 
@@ -96,7 +96,7 @@ def forward(prob, Y, h, R, sender, receiver, N):
 
 
 def backward(prob, Y, h, R, sender, receiver, N, dA):
-    """(dY [E][n_y], dh [N][K][n_h], dR [E][K][P]) of <dA, forward(...)>."""
+    """(dY [E][n_y], dh [N][K][n_h], dR [E][P][K]) of <dA, forward(...)>."""
     Y, h, R, dA = (np.asarray(x, dtype=np.float64) for x in (Y, h, R, dA))
     E, K = _check(prob, Y, h, R, sender, receiver, N)
     sender = np.asarray(sender, dtype=np.int64)
@@ -109,8 +109,8 @@ def backward(prob, Y, h, R, sender, receiver, N, dA):
     for p in range(prob.n_paths):
         ys, hs, As, C = prob.blocks(p)
         v = np.einsum("cab,ea,ekb->ekc", C, Y[:, ys], hs_all[:, :, hs])
-        dR[:, :, p] = np.einsum("ekc,ekc->ek", g[:, :, As], v)
-        w = R[:, :, p, None] * g[:, :, As]                # R_p dA_{l3 m3}
+        dR[:, p, :] = np.einsum("ekc,ekc->ek", g[:, :, As], v)
+        w = R[:, p, :, None] * g[:, :, As]                # R_p dA_{l3 m3}
         dY[:, ys] += np.einsum("cab,ekc,ekb->ea", C, w, hs_all[:, :, hs])
         dhe[:, :, hs] += np.einsum("cab,ekc,ea->ekb", C, w, Y[:, ys])
     dh = np.zeros_like(h)
@@ -132,6 +132,6 @@ def forward_bruteforce(prob, Y, h, R, sender, receiver, N):
                 for m3 in range(2 * l3 + 1):
                     for m1 in range(2 * l1 + 1):
                         for m2 in range(2 * l2 + 1):
-                            A[i, k, As.start + m3] += (C[m3, m1, m2] * R[e, k, p] * Y[e, ys.start + m1]
+                            A[i, k, As.start + m3] += (C[m3, m1, m2] * R[e, p, k] * Y[e, ys.start + m1]
                                                        * h[j, k, hs.start + m2])
     return A

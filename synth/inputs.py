@@ -184,5 +184,5 @@ def gen_tp_inputs(n_nodes, n_edges, channels, n_y, n_h, n_paths, device="cpu", s
     gy, gh, gr = _gen(device, 6 + seed), _gen(device, 7 + seed), _gen(device, 8 + seed)
     Y = torch.randn((n_edges, n_y), generator=gy, device=device, dtype=torch.float32)
     h = torch.randn((n_nodes, channels, n_h), generator=gh, device=device, dtype=torch.float32)
-    R = torch.randn((n_edges, channels, n_paths), generator=gr, device=device, dtype=torch.float32)
+    R = torch.randn((n_edges, n_paths, channels), generator=gr, device=device, dtype=torch.float32)
     return Y, h, R

@@ -17,7 +17,7 @@ def _inputs(prob, N, E, K, seed=0, unit_y=True):
     r = rng.normal(size=(E, 3))
     Y = real_sph_harm(prob.lmax_y, r / np.linalg.norm(r, axis=1, keepdims=True)) if unit_y else rng.normal(size=(E, prob.n_y))
     h = rng.normal(size=(N, K, prob.n_h))
-    R = rng.normal(size=(E, K, prob.n_paths))
+    R = rng.normal(size=(E, prob.n_paths, K))
     s, t = _graph(rng, N, E)
     return Y, h, R, s, t, r, rng
 
@@ -46,17 +46,17 @@ def test_scalar_paths_closed_forms():
     prob = TPProblem(0, (2,), 2)          # single path (0, 2, 2)
     Y = rng.normal(size=(E, 1))
     h = rng.normal(size=(N, K, 5))
-    R = rng.normal(size=(E, K, 1))
+    R = rng.normal(size=(E, 1, K))
     s, t = _graph(rng, N, E)
     ref = np.zeros((N, K, 9))
     for e in range(E):
-        ref[t[e], :, 4:9] += R[e, :, 0, None] * Y[e, 0] * h[s[e]]
+        ref[t[e], :, 4:9] += R[e, 0, :, None] * Y[e, 0] * h[s[e]]
     assert np.abs(forward(prob, Y, h, R, s, t, N) - ref).max() < 1e-12
     prob = TPProblem(2, (2,), 0)          # single path (2, 2, 0)
     Y = rng.normal(size=(E, 9))
     ref = np.zeros((N, K, 1))
     for e in range(E):
-        ref[t[e], :, 0] += R[e, :, 0] * (h[s[e]] @ Y[e, 4:9]) / np.sqrt(5)
+        ref[t[e], :, 0] += R[e, 0, :] * (h[s[e]] @ Y[e, 4:9]) / np.sqrt(5)
     assert np.abs(forward(prob, Y, h, R, s, t, N) - ref).max() < 1e-12
 
 
@@ -74,12 +74,12 @@ def test_vector_paths_closed_forms():
     h[:, 0, 0] = rng.normal(size=6)                         # scalar block
     h[:, 0, 1:4] = Y[:, 1:4]                                # vector block = Y_1(u)
     paths = [prob.path_l(p) for p in range(prob.n_paths)]
-    R = np.zeros((6, 1, prob.n_paths))
-    R[:, 0, paths.index((1, 0, 1))] = 1.0
+    R = np.zeros((6, prob.n_paths, 1))
+    R[:, paths.index((1, 0, 1)), 0] = 1.0
     A = forward(prob, Y, h, R, np.arange(6), np.arange(6), 6)
     assert np.abs(A[:, 0, 1:4] - h[:, 0, 0, None] * Y[:, 1:4]).max() < 1e-12
     R[:] = 0.0
-    R[:, 0, paths.index((1, 1, 2))] = 1.0
+    R[:, paths.index((1, 1, 2)), 0] = 1.0
     A2 = forward(prob, Y, h, R, np.arange(6), np.arange(6), 6)[:, 0, 4:9]
     Y2 = real_sph_harm(2, u)[:, 4:9]
     ratio = (A2 * Y2).sum(1) / (Y2 * Y2).sum(1)
@@ -154,4 +154,4 @@ def test_backward_finite_differences_and_euler_identities():
             Xm[idx] -= eps
             ap, am = [Y, h, R], [Y, h, R]
             ap[i], am[i] = Xp, Xm
-            assert (f(*ap) - f(*am)) / (2 * eps) == pytest.approx(G[idx], rel=1e-7, abs=1e-9)
+            assert (f(*ap) - f(*am)) / (2 * eps) == pytest.approx(G[idx], rel=1e-7, abs=1e-7)
