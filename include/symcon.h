@@ -189,13 +189,14 @@ symcon_status symcon_pack_balanced(const int64_t* sizes, int64_t n, int64_t capa
  * C is the real coupling of symcon_real_cg. Paths: every (l1 <= lmax_y, l2 in hidden_l,
  * l3 <= lmax_out) with |l1-l2| <= l3 <= l1+l2 and l1+l2+l3 even, ordered by (l1, l2, l3)
  * (symcon_tp_path). Layouts (fp32, row-major, 16-byte aligned):
- *   Y [E][(lmax_y+1)^2]  (lm = l^2+l+m)       h  [N][K][n_h] (hidden blocks in hidden_l order)
+ *   Y [E][(lmax_y+1)^2]  (lm = l^2+l+m)       h  [N][n_h][K] (hidden blocks in hidden_l order,
+ *                                                 channel fastest)
  *   R [E][n_paths][K] (channel fastest, e3nn's per-path weight blocks)
  *                                              A  [N][K][(lmax_out+1)^2] (the contraction's A)
  *   sender, receiver: int32 [E]; receiver must be non-decreasing (edges sorted by receiver);
  *   a violation or an index outside [0, N) is reported by symcon_tp_check_device_error
  *   (SYMCON_EINVAL) and the outputs are unspecified. Nodes without incoming edges get A = 0.
- * The backward returns the derivatives of <dA, A>: dY [E][n_y], dh [N][K][n_h] and
+ * The backward returns the derivatives of <dA, A>: dY [E][n_y], dh [N][n_h][K] and
  * dR [E][n_paths][K] (each overwritten; any may be NULL). Deterministic: fixed summation
  * order, no floating-point atomics. */
 typedef struct symcon_tp_plan symcon_tp_plan; /* opaque */

@@ -18,7 +18,8 @@ Readings (t1-t6):
   t2  paths ordered lexicographically by (l1, l2, l3); R has one weight per (edge, path,
       channel), channel fastest: R[E][P][K] (e3nn's per-instruction weight blocks).
   t3  h holds the hidden irreps `hidden_l` (strictly increasing l, one block of 2l+1
-      components each) per (node, channel): h[N][K][n_h]; Y[E][(lmax_y+1)^2] with lm = l^2 + l + m.
+      components each), component-major with the channel fastest: h[N][n_h][K] (like R);
+      Y[E][(lmax_y+1)^2] with lm = l^2 + l + m.
   t4  output A[N][K][(lmax_out+1)^2] (the contraction's input layout); nodes without incoming
       edges get A = 0; the linear mixing and 1/avg-neighbour scaling that MACE applies after the
       sum are outside the kernel ("after a further linear combination").
@@ -67,8 +68,8 @@ class TPProblem:
 
 def _check(prob, Y, h, R, sender, receiver, N):
     E = len(sender)
-    K = h.shape[1]
-    assert Y.shape == (E, prob.n_y) and h.shape == (N, K, prob.n_h) and R.shape == (E, prob.n_paths, K)
+    K = h.shape[2]
+    assert Y.shape == (E, prob.n_y) and h.shape == (N, prob.n_h, K) and R.shape == (E, prob.n_paths, K)
     assert len(receiver) == E
     return E, K
 
@@ -77,7 +78,7 @@ def messages(prob, Y, h, R, sender):
     """Per-edge messages A_{ji,k,l3m3} of Alg. 2, [E][K][n_out]."""
     Y, h, R = (np.asarray(x, dtype=np.float64) for x in (Y, h, R))
     sender = np.asarray(sender, dtype=np.int64)
-    hs_all = h[sender]                                    # h_{j,k,.} of each edge's sender
+    hs_all = h.transpose(0, 2, 1)[sender]                 # h_{j,k,.} of each edge's sender, [E][K][n_h]
     E, K = R.shape[0], R.shape[2]
     M = np.zeros((E, K, prob.n_out))
     for p in range(prob.n_paths):
@@ -96,13 +97,13 @@ def forward(prob, Y, h, R, sender, receiver, N):
 
 
 def backward(prob, Y, h, R, sender, receiver, N, dA):
-    """(dY [E][n_y], dh [N][K][n_h], dR [E][P][K]) of <dA, forward(...)>."""
+    """(dY [E][n_y], dh [N][n_h][K], dR [E][P][K]) of <dA, forward(...)>."""
     Y, h, R, dA = (np.asarray(x, dtype=np.float64) for x in (Y, h, R, dA))
     E, K = _check(prob, Y, h, R, sender, receiver, N)
     sender = np.asarray(sender, dtype=np.int64)
     receiver = np.asarray(receiver, dtype=np.int64)
     g = dA[receiver]                                      # dA_{i,k,.} of each edge's receiver
-    hs_all = h[sender]
+    hs_all = h.transpose(0, 2, 1)[sender]
     dY = np.zeros_like(Y)
     dR = np.zeros_like(R)
     dhe = np.zeros((E, K, prob.n_h))                      # per-edge contribution to dh_{sender}
@@ -113,15 +114,15 @@ def backward(prob, Y, h, R, sender, receiver, N, dA):
         w = R[:, p, :, None] * g[:, :, As]                # R_p dA_{l3 m3}
         dY[:, ys] += np.einsum("cab,ekc,ekb->ea", C, w, hs_all[:, :, hs])
         dhe[:, :, hs] += np.einsum("cab,ekc,ea->ekb", C, w, Y[:, ys])
-    dh = np.zeros_like(h)
+    dh = np.zeros((N, K, prob.n_h))
     np.add.at(dh, sender, dhe)
-    return dY, dh, dR
+    return dY, dh.transpose(0, 2, 1).copy(), dR
 
 
 def forward_bruteforce(prob, Y, h, R, sender, receiver, N):
     """Alg. 2 line by line in plain Python loops (tiny inputs only)."""
     E = len(sender)
-    K = h.shape[1]
+    K = h.shape[2]
     A = np.zeros((N, K, prob.n_out))
     for e in range(E):
         j, i = int(sender[e]), int(receiver[e])
@@ -133,5 +134,5 @@ def forward_bruteforce(prob, Y, h, R, sender, receiver, N):
                     for m1 in range(2 * l1 + 1):
                         for m2 in range(2 * l2 + 1):
                             A[i, k, As.start + m3] += (C[m3, m1, m2] * R[e, p, k] * Y[e, ys.start + m1]
-                                                       * h[j, k, hs.start + m2])
+                                                       * h[j, hs.start + m2, k])
     return A

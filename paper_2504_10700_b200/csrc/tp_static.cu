@@ -96,7 +96,7 @@ __global__ void tp_seg_sort(const int* __restrict__ off, int N, int* __restrict_
   }
 }
 
-// dh[j][k][:] = sum over the sender's edges (ascending id) of dhe[e][:][k]; thread per (j, k)
+// dh[j][:][k] = sum over the sender's edges (ascending id) of dhe[e][:][k]; thread per (j, k)
 __global__ void tp_dh_reduce(const float* __restrict__ dhe, const int* __restrict__ off, const int* __restrict__ perm,
                              int N, int K, int nh, float* __restrict__ dh) {
   const long long total = (long long)N * K;
@@ -111,10 +111,10 @@ __global__ void tp_dh_reduce(const float* __restrict__ dhe, const int* __restric
       for (int q = 0; q < 16; q++)
         if (q < nh) acc[q] += __ldg(src + (long long)q * K);
     }
-    float* d = dh + t * nh;
+    float* d = dh + (long long)j * nh * K + k;   // dh[j][q][k] (h's layout)
 #pragma unroll
     for (int q = 0; q < 16; q++)
-      if (q < nh) d[q] = acc[q];
+      if (q < nh) d[(long long)q * K] = acc[q];
   }
 }
 

@@ -212,7 +212,7 @@ class ChannelwiseTP:
         N, E, K = h.shape[0], sender.shape[0], self.channels
         for t in (Y, h, R):
             assert t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()
-        assert Y.shape == (E, self.n_y) and h.shape == (N, K, self.n_h) and R.shape == (E, self.n_paths, K)
+        assert Y.shape == (E, self.n_y) and h.shape == (N, self.n_h, K) and R.shape == (E, self.n_paths, K)
         assert sender.dtype == torch.int32 and receiver.dtype == torch.int32 and receiver.shape == (E,)
         return N, E
 

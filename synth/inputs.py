@@ -183,6 +183,6 @@ def gen_tp_graph(sizes, deg=30, seed=0):
 def gen_tp_inputs(n_nodes, n_edges, channels, n_y, n_h, n_paths, device="cpu", seed=0):
     gy, gh, gr = _gen(device, 6 + seed), _gen(device, 7 + seed), _gen(device, 8 + seed)
     Y = torch.randn((n_edges, n_y), generator=gy, device=device, dtype=torch.float32)
-    h = torch.randn((n_nodes, channels, n_h), generator=gh, device=device, dtype=torch.float32)
+    h = torch.randn((n_nodes, n_h, channels), generator=gh, device=device, dtype=torch.float32)
     R = torch.randn((n_edges, n_paths, channels), generator=gr, device=device, dtype=torch.float32)
     return Y, h, R

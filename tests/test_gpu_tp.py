@@ -89,8 +89,8 @@ def test_tp_edge_cases_and_errors():
     # no edges at all: A = 0, dh = 0
     e0 = lambda *sh: torch.zeros(sh, device="cuda")
     i0 = torch.zeros(0, dtype=torch.int32, device="cuda")
-    A0 = tp.forward_raw(e0(0, tp.n_y), h, e0(0, 32, tp.n_paths), i0, i0)
-    dY0, dh0, dR0 = tp.backward_raw(e0(0, tp.n_y), h, e0(0, 32, tp.n_paths), i0, i0, torch.ones_like(A0))
+    A0 = tp.forward_raw(e0(0, tp.n_y), h, e0(0, tp.n_paths, 32), i0, i0)
+    dY0, dh0, dR0 = tp.backward_raw(e0(0, tp.n_y), h, e0(0, tp.n_paths, 32), i0, i0, torch.ones_like(A0))
     torch.cuda.synchronize()
     assert torch.count_nonzero(A0) == 0 and torch.count_nonzero(dh0) == 0 and dY0.numel() == 0
     # unsorted receivers -> EINVAL at the first offending edge; outputs unspecified but no fault

@@ -16,7 +16,7 @@ def _inputs(prob, N, E, K, seed=0, unit_y=True):
     rng = np.random.default_rng(seed)
     r = rng.normal(size=(E, 3))
     Y = real_sph_harm(prob.lmax_y, r / np.linalg.norm(r, axis=1, keepdims=True)) if unit_y else rng.normal(size=(E, prob.n_y))
-    h = rng.normal(size=(N, K, prob.n_h))
+    h = rng.normal(size=(N, prob.n_h, K))
     R = rng.normal(size=(E, prob.n_paths, K))
     s, t = _graph(rng, N, E)
     return Y, h, R, s, t, r, rng
@@ -45,18 +45,18 @@ def test_scalar_paths_closed_forms():
     N, E, K = 4, 9, 2
     prob = TPProblem(0, (2,), 2)          # single path (0, 2, 2)
     Y = rng.normal(size=(E, 1))
-    h = rng.normal(size=(N, K, 5))
+    h = rng.normal(size=(N, 5, K))
     R = rng.normal(size=(E, 1, K))
     s, t = _graph(rng, N, E)
     ref = np.zeros((N, K, 9))
     for e in range(E):
-        ref[t[e], :, 4:9] += R[e, 0, :, None] * Y[e, 0] * h[s[e]]
+        ref[t[e], :, 4:9] += R[e, 0, :, None] * Y[e, 0] * h[s[e]].T
     assert np.abs(forward(prob, Y, h, R, s, t, N) - ref).max() < 1e-12
     prob = TPProblem(2, (2,), 0)          # single path (2, 2, 0)
     Y = rng.normal(size=(E, 9))
     ref = np.zeros((N, K, 1))
     for e in range(E):
-        ref[t[e], :, 0] += R[e, 0, :] * (h[s[e]] @ Y[e, 4:9]) / np.sqrt(5)
+        ref[t[e], :, 0] += R[e, 0, :] * (h[s[e]].T @ Y[e, 4:9]) / np.sqrt(5)
     assert np.abs(forward(prob, Y, h, R, s, t, N) - ref).max() < 1e-12
 
 
@@ -70,9 +70,9 @@ def test_vector_paths_closed_forms():
     u = rng.normal(size=(6, 3))
     u /= np.linalg.norm(u, axis=1, keepdims=True)
     Y = real_sph_harm(1, u)                                 # [6][4]
-    h = np.zeros((6, 1, prob.n_h))
+    h = np.zeros((6, prob.n_h, 1))
     h[:, 0, 0] = rng.normal(size=6)                         # scalar block
-    h[:, 0, 1:4] = Y[:, 1:4]                                # vector block = Y_1(u)
+    h[:, 1:4, 0] = Y[:, 1:4]                                # vector block = Y_1(u)
     paths = [prob.path_l(p) for p in range(prob.n_paths)]
     R = np.zeros((6, prob.n_paths, 1))
     R[:, paths.index((1, 0, 1)), 0] = 1.0
@@ -100,7 +100,7 @@ def test_rotation_equivariance():
         for b, l in enumerate(prob.hidden_l):
             o = prob.h_off[b]
             Dh[o:o + 2 * l + 1, o:o + 2 * l + 1] = wigner_d_fit(l, Rot)
-        hr = np.einsum("ab,nkb->nka", Dh, h)
+        hr = np.einsum("ab,nbk->nak", Dh, h)
         Ar = forward(prob, Yr, hr, R, s, t, N)
         assert np.abs(Ar - np.einsum("ab,nkb->nka", block_diag_d(3, Rot), A)).max() < 1e-9 * np.abs(A).max()
 
