@@ -96,25 +96,50 @@ __global__ void tp_seg_sort(const int* __restrict__ off, int N, int* __restrict_
   }
 }
 
-// dh[j][:][k] = sum over the sender's edges (ascending id) of dhe[e][:][k]; thread per (j, k)
+// dh[j][:][k] = sum over the sender's edges (ascending id) of dhe[e][:][k]; thread per (j, channel
+// pair) with 8-byte loads (K even) or per (j, channel); the edge indices of the next group of 4
+// edges are loaded before their rows (independent loads in flight), summation order fixed.
+template <int CPT>
 __global__ void tp_dh_reduce(const float* __restrict__ dhe, const int* __restrict__ off, const int* __restrict__ perm,
                              int N, int K, int nh, float* __restrict__ dh) {
-  const long long total = (long long)N * K;
+  const int KT = K / CPT;
+  const long long total = (long long)N * KT;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
-    const int j = (int)(t / K), k = (int)(t - (long long)j * K);
-    float acc[16];
+    const int j = (int)(t / KT), k = (int)(t - (long long)j * KT) * CPT;
+    float acc[16][CPT];
 #pragma unroll
-    for (int q = 0; q < 16; q++) acc[q] = 0.f;
-    for (int s = off[j]; s < off[j + 1]; s++) {
-      const float* src = dhe + (long long)perm[s] * nh * K + k;   // dhe[e][q][k]: coalesced over k
+    for (int q = 0; q < 16; q++)
 #pragma unroll
-      for (int q = 0; q < 16; q++)
-        if (q < nh) acc[q] += __ldg(src + (long long)q * K);
+      for (int c = 0; c < CPT; c++) acc[q][c] = 0.f;
+    const int a = off[j], b = off[j + 1];
+    for (int s0 = a; s0 < b; s0 += 4) {
+      int ev[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) ev[u] = (s0 + u < b) ? perm[s0 + u] : -1;
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        if (ev[u] < 0) continue;
+        const float* src = dhe + (long long)ev[u] * nh * K + k;
+#pragma unroll
+        for (int q = 0; q < 16; q++) {
+          if (q >= nh) break;
+          if (CPT == 2) {
+            const float2 v = __ldg(reinterpret_cast<const float2*>(src + (long long)q * K));
+            acc[q][0] += v.x;
+            acc[q][CPT - 1] += v.y;
+          } else {
+            acc[q][0] += __ldg(src + (long long)q * K);
+          }
+        }
+      }
     }
     float* d = dh + (long long)j * nh * K + k;   // dh[j][q][k] (h's layout)
 #pragma unroll
-    for (int q = 0; q < 16; q++)
-      if (q < nh) d[(long long)q * K] = acc[q];
+    for (int q = 0; q < 16; q++) {
+      if (q >= nh) break;
+      if (CPT == 2) *reinterpret_cast<float2*>(d + (long long)q * K) = make_float2(acc[q][0], acc[q][CPT - 1]);
+      else d[(long long)q * K] = acc[q][0];
+    }
   }
 }
 
@@ -151,7 +176,10 @@ int tp_csr_launch(const TPCsrArgs& a, cudaStream_t st) {
 int tp_dh_reduce_launch(const float* dhe, const int* off, const int* perm, int N, int K, int nh, float* dh,
                         cudaStream_t st) {
   if (N <= 0) return 0;
-  tp_dh_reduce<<<grid_for((long long)N * K, 256), 256, 0, st>>>(dhe, off, perm, N, K, nh, dh);
+  if (K % 2 == 0)
+    tp_dh_reduce<2><<<grid_for((long long)N * K / 2, 256), 256, 0, st>>>(dhe, off, perm, N, K, nh, dh);
+  else
+    tp_dh_reduce<1><<<grid_for((long long)N * K, 256), 256, 0, st>>>(dhe, off, perm, N, K, nh, dh);
   return 1;
 }
 

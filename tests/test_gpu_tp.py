@@ -38,6 +38,8 @@ def _host(*ts):
     ("ragged_K13", 2, (0, 1), 2, 13, [17, 9, 30]),
     ("lmax_y1_out1", 1, (1,), 1, 40, [8, 8, 8]),
     ("hidden_0123", 3, (0, 1, 2, 3), 3, 33, [12, 20]),
+    ("even_K6", 3, (0, 1), 3, 6, [9, 14]),            # channel pairs with 8-byte async chunks
+    ("K96_ragged_pairs", 2, (0, 1), 2, 96, [20, 25]),  # last 64-channel group half full
 ])
 def test_tp_against_oracle(name, lmax_y, hidden, lmax_out, K, sizes):
     from oracle.tp import TPProblem, forward, backward
