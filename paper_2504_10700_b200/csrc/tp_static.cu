@@ -123,7 +123,13 @@ __global__ void tp_dh_reduce(const float* __restrict__ dhe, const int* __restric
 #pragma unroll
         for (int q = 0; q < 16; q++) {
           if (q >= nh) break;
-          if (CPT == 2) {
+          if (CPT == 4) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(src + (long long)q * K));
+            acc[q][0] += v.x;
+            acc[q][1 % CPT] += v.y;
+            acc[q][2 % CPT] += v.z;
+            acc[q][3 % CPT] += v.w;
+          } else if (CPT == 2) {
             const float2 v = __ldg(reinterpret_cast<const float2*>(src + (long long)q * K));
             acc[q][0] += v.x;
             acc[q][CPT - 1] += v.y;
@@ -137,7 +143,9 @@ __global__ void tp_dh_reduce(const float* __restrict__ dhe, const int* __restric
 #pragma unroll
     for (int q = 0; q < 16; q++) {
       if (q >= nh) break;
-      if (CPT == 2) *reinterpret_cast<float2*>(d + (long long)q * K) = make_float2(acc[q][0], acc[q][CPT - 1]);
+      if (CPT == 4)
+        *reinterpret_cast<float4*>(d + (long long)q * K) = make_float4(acc[q][0], acc[q][1 % CPT], acc[q][2 % CPT], acc[q][3 % CPT]);
+      else if (CPT == 2) *reinterpret_cast<float2*>(d + (long long)q * K) = make_float2(acc[q][0], acc[q][CPT - 1]);
       else d[(long long)q * K] = acc[q][0];
     }
   }
@@ -176,7 +184,9 @@ int tp_csr_launch(const TPCsrArgs& a, cudaStream_t st) {
 int tp_dh_reduce_launch(const float* dhe, const int* off, const int* perm, int N, int K, int nh, float* dh,
                         cudaStream_t st) {
   if (N <= 0) return 0;
-  if (K % 2 == 0)
+  if (K % 4 == 0)
+    tp_dh_reduce<4><<<grid_for((long long)N * K / 4, 256), 256, 0, st>>>(dhe, off, perm, N, K, nh, dh);
+  else if (K % 2 == 0)
     tp_dh_reduce<2><<<grid_for((long long)N * K / 2, 256), 256, 0, st>>>(dhe, off, perm, N, K, nh, dh);
   else
     tp_dh_reduce<1><<<grid_for((long long)N * K, 256), 256, 0, st>>>(dhe, off, perm, N, K, nh, dh);
