@@ -41,6 +41,7 @@ struct TPCsrArgs {
   int* send_off;            // [N+1]
   int* send_cur;            // [N]
   int* send_perm;           // [E]
+  int* send_pos;            // [E] position of edge e in the sender CSR (inverse of send_perm)
 };
 int tp_csr_launch(const TPCsrArgs& a, cudaStream_t st);
 int tp_dh_reduce_launch(const float* dhe, const int* off, const int* perm, int N, int K, int nh, float* dh,

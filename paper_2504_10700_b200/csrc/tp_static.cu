@@ -96,9 +96,9 @@ __global__ void tp_seg_sort(const int* __restrict__ off, int N, int* __restrict_
   }
 }
 
-// dh[j][:][k] = sum over the sender's edges (ascending id) of dhe[e][:][k]; thread per (j, channel
-// pair) with 8-byte loads (K even) or per (j, channel); the edge indices of the next group of 4
-// edges are loaded before their rows (independent loads in flight), summation order fixed.
+// dh[j][:][k] = sum over the sender's edges (ascending id) of their dhe rows, which the backward
+// kernel wrote at the edge's position in the sender CSR (contiguous per sender); thread per (j,
+// channel pair) with 8-byte loads (K even) or per (j, channel); summation order fixed.
 template <int CPT>
 __global__ void tp_dh_reduce(const float* __restrict__ dhe, const int* __restrict__ off, const int* __restrict__ perm,
                              int N, int K, int nh, float* __restrict__ dh) {
@@ -113,13 +113,12 @@ __global__ void tp_dh_reduce(const float* __restrict__ dhe, const int* __restric
       for (int c = 0; c < CPT; c++) acc[q][c] = 0.f;
     const int a = off[j], b = off[j + 1];
     for (int s0 = a; s0 < b; s0 += 4) {
-      int ev[4];
-#pragma unroll
-      for (int u = 0; u < 4; u++) ev[u] = (s0 + u < b) ? perm[s0 + u] : -1;
 #pragma unroll
       for (int u = 0; u < 4; u++) {
-        if (ev[u] < 0) continue;
-        const float* src = dhe + (long long)ev[u] * nh * K + k;
+        if (s0 + u >= b) break;
+        // dhe rows are stored in sender-CSR order (row = position of the edge in the sender's
+        // sorted list): a sender's rows are contiguous and are read as one stream
+        const float* src = dhe + (long long)(s0 + u) * nh * K + k;
 #pragma unroll
         for (int q = 0; q < 16; q++) {
           if (q >= nh) break;
@@ -151,6 +150,10 @@ __global__ void tp_dh_reduce(const float* __restrict__ dhe, const int* __restric
   }
 }
 
+__global__ void tp_inv_perm(const int* __restrict__ perm, int E, int* __restrict__ pos) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < E; q += gridDim.x * blockDim.x) pos[perm[q]] = q;
+}
+
 int grid_for(long long n, int threads) {
   long long b = (n + threads - 1) / threads;
   return (int)(b < 1 ? 1 : (b > 148 * 32 ? 148 * 32 : b));
@@ -175,7 +178,8 @@ int tp_csr_launch(const TPCsrArgs& a, cudaStream_t st) {
     if (a.E > 0) {
       tp_send_scatter<<<grid_for(a.E, 256), 256, 0, st>>>(a.sender, a.N, a.E, a.send_cur, a.send_perm);
       tp_seg_sort<<<grid_for(a.N, 128), 128, 0, st>>>(a.send_off, a.N, a.send_perm);
-      n += 2;
+      tp_inv_perm<<<grid_for(a.E, 256), 256, 0, st>>>(a.send_perm, a.E, a.send_pos);
+      n += 3;
     }
   }
   return n;
@@ -184,9 +188,7 @@ int tp_csr_launch(const TPCsrArgs& a, cudaStream_t st) {
 int tp_dh_reduce_launch(const float* dhe, const int* off, const int* perm, int N, int K, int nh, float* dh,
                         cudaStream_t st) {
   if (N <= 0) return 0;
-  if (K % 4 == 0)
-    tp_dh_reduce<4><<<grid_for((long long)N * K / 4, 256), 256, 0, st>>>(dhe, off, perm, N, K, nh, dh);
-  else if (K % 2 == 0)
+  if (K % 2 == 0)
     tp_dh_reduce<2><<<grid_for((long long)N * K / 2, 256), 256, 0, st>>>(dhe, off, perm, N, K, nh, dh);
   else
     tp_dh_reduce<1><<<grid_for((long long)N * K, 256), 256, 0, st>>>(dhe, off, perm, N, K, nh, dh);
