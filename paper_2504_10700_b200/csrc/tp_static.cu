@@ -99,52 +99,47 @@ __global__ void tp_seg_sort(const int* __restrict__ off, int N, int* __restrict_
 // dh[j][:][k] = sum over the sender's edges (ascending id) of their dhe rows, which the backward
 // kernel wrote at the edge's position in the sender CSR (contiguous per sender); thread per (j,
 // channel pair) with 8-byte loads (K even) or per (j, channel); summation order fixed.
-template <int CPT>
-__global__ void tp_dh_reduce(const float* __restrict__ dhe, const int* __restrict__ off, const int* __restrict__ perm,
-                             int N, int K, int nh, float* __restrict__ dh) {
+template <int CPT, int NH>
+__global__ void tp_dh_reduce(const float* __restrict__ dhe, const int* __restrict__ off, int N, int K,
+                             float* __restrict__ dh) {
   const int KT = K / CPT;
   const long long total = (long long)N * KT;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
     const int j = (int)(t / KT), k = (int)(t - (long long)j * KT) * CPT;
-    float acc[16][CPT];
+    float acc[NH][CPT];
 #pragma unroll
-    for (int q = 0; q < 16; q++)
+    for (int q = 0; q < NH; q++)
 #pragma unroll
       for (int c = 0; c < CPT; c++) acc[q][c] = 0.f;
     const int a = off[j], b = off[j + 1];
     for (int s0 = a; s0 < b; s0 += 4) {
+      float v[4][NH][CPT];
 #pragma unroll
       for (int u = 0; u < 4; u++) {
-        if (s0 + u >= b) break;
-        // dhe rows are stored in sender-CSR order (row = position of the edge in the sender's
-        // sorted list): a sender's rows are contiguous and are read as one stream
-        const float* src = dhe + (long long)(s0 + u) * nh * K + k;
+        const bool ok = s0 + u < b;
+        const float* src = dhe + (long long)(ok ? s0 + u : a) * NH * K + k;
 #pragma unroll
-        for (int q = 0; q < 16; q++) {
-          if (q >= nh) break;
-          if (CPT == 4) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(src + (long long)q * K));
-            acc[q][0] += v.x;
-            acc[q][1 % CPT] += v.y;
-            acc[q][2 % CPT] += v.z;
-            acc[q][3 % CPT] += v.w;
-          } else if (CPT == 2) {
-            const float2 v = __ldg(reinterpret_cast<const float2*>(src + (long long)q * K));
-            acc[q][0] += v.x;
-            acc[q][CPT - 1] += v.y;
+        for (int q = 0; q < NH; q++) {
+          if (CPT == 2) {
+            const float2 x = ok ? __ldg(reinterpret_cast<const float2*>(src + (long long)q * K)) : make_float2(0.f, 0.f);
+            v[u][q][0] = x.x;
+            v[u][q][CPT - 1] = x.y;
           } else {
-            acc[q][0] += __ldg(src + (long long)q * K);
+            v[u][q][0] = ok ? __ldg(src + (long long)q * K) : 0.f;
           }
         }
       }
-    }
-    float* d = dh + (long long)j * nh * K + k;   // dh[j][q][k] (h's layout)
 #pragma unroll
-    for (int q = 0; q < 16; q++) {
-      if (q >= nh) break;
-      if (CPT == 4)
-        *reinterpret_cast<float4*>(d + (long long)q * K) = make_float4(acc[q][0], acc[q][1 % CPT], acc[q][2 % CPT], acc[q][3 % CPT]);
-      else if (CPT == 2) *reinterpret_cast<float2*>(d + (long long)q * K) = make_float2(acc[q][0], acc[q][CPT - 1]);
+      for (int u = 0; u < 4; u++)
+#pragma unroll
+        for (int q = 0; q < NH; q++)
+#pragma unroll
+          for (int c = 0; c < CPT; c++) acc[q][c] += v[u][q][c];
+    }
+    float* d = dh + (long long)j * NH * K + k;   // dh[j][q][k] (h's layout)
+#pragma unroll
+    for (int q = 0; q < NH; q++) {
+      if (CPT == 2) *reinterpret_cast<float2*>(d + (long long)q * K) = make_float2(acc[q][0], acc[q][CPT - 1]);
       else d[(long long)q * K] = acc[q][0];
     }
   }
@@ -187,11 +182,22 @@ int tp_csr_launch(const TPCsrArgs& a, cudaStream_t st) {
 
 int tp_dh_reduce_launch(const float* dhe, const int* off, const int* perm, int N, int K, int nh, float* dh,
                         cudaStream_t st) {
+  (void)perm;
   if (N <= 0) return 0;
-  if (K % 2 == 0)
-    tp_dh_reduce<2><<<grid_for((long long)N * K / 2, 256), 256, 0, st>>>(dhe, off, perm, N, K, nh, dh);
-  else
-    tp_dh_reduce<1><<<grid_for((long long)N * K, 256), 256, 0, st>>>(dhe, off, perm, N, K, nh, dh);
+  const bool pr = K % 2 == 0;
+  const int g = grid_for((long long)N * K / (pr ? 2 : 1), 256);
+#define TP_DH_CASE(NHV)                                                                  \
+  case NHV:                                                                              \
+    if (pr) tp_dh_reduce<2, NHV><<<g, 256, 0, st>>>(dhe, off, N, K, dh);                 \
+    else tp_dh_reduce<1, NHV><<<g, 256, 0, st>>>(dhe, off, N, K, dh);                    \
+    break;
+  switch (nh) {
+    TP_DH_CASE(1) TP_DH_CASE(2) TP_DH_CASE(3) TP_DH_CASE(4) TP_DH_CASE(5) TP_DH_CASE(6) TP_DH_CASE(7) TP_DH_CASE(8)
+    TP_DH_CASE(9) TP_DH_CASE(10) TP_DH_CASE(11) TP_DH_CASE(12) TP_DH_CASE(13) TP_DH_CASE(14) TP_DH_CASE(15)
+    TP_DH_CASE(16)
+    default: return 0;
+  }
+#undef TP_DH_CASE
   return 1;
 }
 
