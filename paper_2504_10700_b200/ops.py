@@ -206,6 +206,7 @@ class ChannelwiseTP:
         nbytes = _lib.symcon_tp_workspace_bytes(self.plan, N, E)
         if self._ws is None or self._ws.numel() < nbytes:
             self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+            self._ws[:8].fill_(255)   # error word = "no error" until a call writes it
         return self._ws
 
     def _check(self, Y, h, R, sender, receiver):
