@@ -304,8 +304,8 @@ static symcon_status build_common(int lmax_in, int corr, const int* out_L, int n
   p->npad = (int)((p->t.rows.size() + 31) / 32 * 32);
   // measured defaults (profiles/r01): few large row groups when the dB row is short (MP-medium:
   // 52 rows x 8 warps, fewer smem reads per FMA), smaller groups for the 9-output large shape
-  if (p->kc.dw_rows_per_group <= 0) p->kc.dw_rows_per_group = p->t.out_per_ch > 4 ? 26 : 52;
-  if (p->kc.dw_groups_per_cta <= 0) p->kc.dw_groups_per_cta = p->t.out_per_ch > 4 ? 16 : 8;
+  if (p->kc.dw_rows_per_group <= 0) p->kc.dw_rows_per_group = p->t.out_per_ch > 4 ? 56 : 52;
+  if (p->kc.dw_groups_per_cta <= 0) p->kc.dw_groups_per_cta = 8;
   // W_bar also holds the JVP direction rows in registers: at most 8 warps (255 registers each)
   // (and enough warps that the register staging of A, U and dB stays small)
   if (p->kc.dw2_rows_per_group <= 0) {
