@@ -113,6 +113,25 @@ def alg_ops(sc):
             "prefixes": len(prefixes), "deg3_monomials": deg3, "n_sym": int(len(L))}
 
 
+def path_roofline(cfg, sc, mean_nodes, path_ops, ms_step, dbl):
+    """Whole-step roofline: the step's algorithmic FP32 lane-ops at the ALU peak vs its
+    algorithmic HBM bytes at the measured copy bandwidth (A read twice, dB, B and dA
+    once per node-channel; the double backward adds uA, A, dB reads and dB_bar, A_bar writes)."""
+    K = cfg.channels
+    nlm = (cfg.lmax_in + 1) ** 2
+    outc = sc.out_dim // K
+    per = 4 * (2 * nlm + outc + outc + nlm)
+    if dbl:
+        per += 4 * (3 * nlm + outc + outc + nlm)
+    hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6553.0
+    t_alu = path_ops / (148 * 128 * 1.965e9)
+    t_hbm = per * mean_nodes * K / (hbm * 1e9)
+    bound = "alu" if t_alu >= t_hbm else "hbm"
+    return {"bound": bound, "frac": max(t_alu, t_hbm) / (ms_step / 1e3), "t_alu_ms": t_alu * 1e3, "t_hbm_ms": t_hbm * 1e3,
+            "bytes_per_node_channel": per}
+
+
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
     """SM clock and throttle reasons sampled DURING the timed region: an NVML thread polls every
@@ -461,6 +480,7 @@ def run_ours(args):
             "per_gpu_nodes_per_s": value / world,
             "path_tops": path_ops / (ms_max / args.steps / 1e3) / 1e12,
             "path_frac_of_alu_peak": path_ops / (ms_max / args.steps / 1e3) / 1e12 / (148 * 128 * 1.965e-3),
+            "path_roofline": path_roofline(cfg, sc, nodes / args.steps, path_ops, ms_max / args.steps, args.double_backward),
             "roofline": roof, "kernels": kernels, "alg_ops_per_node_channel": ops,
             "clocks": clocks, "gpu_launches": launches_timed,
             "kernel_timing": "per-kernel CUDA events from a separate pass of the same steps with dW and dA back to back",
