@@ -133,10 +133,36 @@ def path_roofline(cfg, sc, mean_nodes, path_ops, ms_step, dbl):
 
 
 # ----------------------------------------------------------------------------- clocks
+_CLOCK_CHILD = r"""
+import json, select, sys, time
+try:
+    import pynvml
+    pynvml.nvmlInit()
+    h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+    mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+except Exception:
+    try:
+        print(json.dumps({"ready": None}), flush=True)
+        sys.stdin.readline()
+        print(json.dumps([]), flush=True)
+    except Exception:
+        pass
+    sys.exit(0)
+print(json.dumps({"ready": mx}), flush=True)
+out = []
+while not select.select([sys.stdin], [], [], 0)[0]:
+    out.append((time.time(), pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
+    time.sleep(0.002)
+sys.stdin.readline()
+print(json.dumps(out), flush=True)
+"""
+
+
 class ClockSampler:
-    """SM clock and throttle reasons sampled DURING the timed region: an NVML thread polls every
-    ~2 ms from before the region starts; samples are kept if they fall inside [start, end]
-    (marked by the caller) widened by 20 ms."""
+    """SM clock and throttle reasons sampled DURING the timed region by a separate sampler process
+    (no GIL contention with the launching thread) polling NVML every ~2 ms from before the region
+    starts; samples are kept if they fall inside [start, end] (marked by the caller) widened by 20 ms."""
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4,
                "hw_power_brake_slowdown": 0x80}
 
@@ -144,57 +170,46 @@ class ClockSampler:
         self.index = index
         self.samples = []          # (t, mhz, reasons)
         self.max_mhz = None
-        self._stop = threading.Event()
-        self._ready = threading.Event()
-        self._t = None
+        self._p = None
         self.t0 = self.t1 = None
-
-    def _run(self):
-        import pynvml
-        try:
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
-        finally:
-            self._ready.set()
-        while not self._stop.is_set():
-            mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-            r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-            self.samples.append((time.perf_counter(), mhz, r))
-            time.sleep(0.002)
 
     def __enter__(self):
         try:
-            import pynvml
-            pynvml.nvmlInit()
-            self._t = threading.Thread(target=self._run, daemon=True)
-            self._t.start()
-            self._ready.wait(timeout=5)
-            time.sleep(0.01)
+            self._p = subprocess.Popen([sys.executable, "-c", _CLOCK_CHILD, str(self.index)], stdin=subprocess.PIPE,
+                                       stdout=subprocess.PIPE, text=True)
+            self.max_mhz = json.loads(self._p.stdout.readline())["ready"]
+            time.sleep(0.02)
         except Exception:  # noqa: BLE001
-            self._t = None
+            self._p = None
         return self
 
+    def __exit__(self, *a):
+        if self._p is None:
+            return
+        time.sleep(0.02)
+        try:
+            self._p.stdin.write("stop\n")
+            self._p.stdin.flush()
+            self.samples = [tuple(x) for x in json.loads(self._p.stdout.readline())]
+        except Exception:  # noqa: BLE001
+            pass
+        self._p.wait(timeout=10)
+
     def start(self):
-        self.t0 = time.perf_counter()
+        self.t0 = time.time()
 
     def end(self):
-        self.t1 = time.perf_counter()
-
-    def __exit__(self, *a):
-        time.sleep(0.01)
-        self._stop.set()
-        if self._t:
-            self._t.join(timeout=2)
+        self.t1 = time.time()
 
     def summary(self):
         t0 = (self.t0 or 0) - 0.02
-        t1 = (self.t1 or time.perf_counter()) + 0.02
+        t1 = (self.t1 or time.time()) + 0.02
         win = [(m, r) for (t, m, r) in self.samples if t0 <= t <= t1]
         mx = self.max_mhz
         sm = [m for m, _ in win]
         reasons = sorted({name for _, r in win for name, bit in self.REASONS.items() if r & bit})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_min_mhz": min(sm) if sm else None,
-                "sm_max_mhz": mx, "reasons": reasons, "samples": len(sm), "source": "nvml ~2ms"}
+                "sm_max_mhz": mx, "reasons": reasons, "samples": len(sm), "source": "nvml ~2ms (sampler process)"}
 
 
 # ----------------------------------------------------------------------------- cpu oracle
