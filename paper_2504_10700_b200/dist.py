@@ -54,9 +54,11 @@ class DataParallelContraction:
         self.group = group
         self.overlap = overlap
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
-        # measured (profiles/r01): concurrent dW/dA helps at N=1 (+4%); with N>1 the NCCL all-reduce
-        # kernels compete for the same SMs and the sequential dW -> (all-reduce || dA) order is better
-        self.concurrent_bwd = (self.world == 1) if concurrent_bwd is None else concurrent_bwd
+        # measured (profiles/r01): concurrent dW/dA helps at N=1 (+2-4%); at N=2/4 the sequential
+        # dW -> (all-reduce || dA) order is erratic (the NCCL kernel becomes ready together with the
+        # persistent dA grid and waits for SMs while its peers spin: 1.3-4.6 ms per step), while dA
+        # started together with dW leaves the all-reduce to run as SMs free up: stable 1.30 ms at N=2
+        self.concurrent_bwd = True if concurrent_bwd is None else concurrent_bwd
         self.side = torch.cuda.Stream(device=sc.device) if self.concurrent_bwd else None
         self.comm = torch.cuda.Stream(device=sc.device) if self.world > 1 else None
         self.launches = 0
