@@ -371,7 +371,8 @@ symcon_status symcon_build_tables(int lmax_in, int correlation, const int* out_L
                                                                          p->tile_smem), "occupancy bwd2");
       p->grid_bwd2 = sms * std::max(occ_2, 1);
       p->grid_fwd = sms * std::max(occ_f, 1);
-      p->grid_dA = sms * std::max(p->kc.da_ctas_per_sm > 0 ? std::min(occ_a, p->kc.da_ctas_per_sm) : occ_a, 1);
+      p->grid_dA = std::max(1, sms - std::max(0, p->kc.da_reserve_sms)) *
+                   std::max(p->kc.da_ctas_per_sm > 0 ? std::min(occ_a, p->kc.da_ctas_per_sm) : occ_a, 1);
     }
     {
       const int nout = p->t.out_per_ch, nrows = (int)p->t.rows.size();

@@ -65,6 +65,7 @@ struct KernelConfig {
   int dw_rows_per_group = 0;       // transposed dW: rows j per warp (register accumulators); 0 = auto
   int dw_groups_per_cta = 0;       // transposed dW: warps per CTA; 0 = auto
   int bwd2_min_blocks = 10;        // double backward tile kernel: __launch_bounds__ min blocks (caps registers)
+  int da_reserve_sms = 0;          // dA persistent grid leaves this many SMs free (for NCCL kernels at N > 1)
   int da_ctas_per_sm = 0;          // dA persistent grid: CTAs per SM (0 = occupancy maximum); fewer leave
                                    // room for concurrent dW CTAs on the same SMs
   int dw2_rows_per_group = 0;      // double-backward W_bar kernel (same layout): rows per warp; 0 = auto
