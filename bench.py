@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=32768, help="nodes in the oracle's bounded sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-overlap", action="store_true", help="all-reduce dW after dA instead of overlapping")
+    ap.add_argument("--allreduce", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: dW all-reduce by libsymcon's NVLink peer-memory kernel (default) or NCCL")
     ap.add_argument("--sequential-bwd", action="store_true", help="run the dW and dA kernels back to back on one stream")
     ap.add_argument("--concurrent-bwd", action="store_true", help="run dA on a side stream concurrent with dW (default at N=1)")
     ap.add_argument("--channelwise-tp", action="store_true",
@@ -323,7 +325,7 @@ def run_ours(args):
     for q in range(POOL):
         sc.workspace(pool[q][1])
     conc = False if args.sequential_bwd else (True if args.concurrent_bwd else None)
-    dp = DataParallelContraction(sc, overlap=not args.no_overlap, concurrent_bwd=conc)
+    dp = DataParallelContraction(sc, overlap=not args.no_overlap, concurrent_bwd=conc, allreduce=args.allreduce)
 
     def bwd2(q, A, ne, dB, runner):
         # double backward of the same step (force loss): uA terms through symcon_backward2, W_bar
@@ -365,7 +367,7 @@ def run_ours(args):
     # stream (the throughput region above overlaps dW and dA, which would blur each kernel's time)
     _lib.symcon_profile_enable(sc.plan, 1)
     _lib.symcon_profile_reset(sc.plan)
-    seq = DataParallelContraction(sc, overlap=not args.no_overlap, concurrent_bwd=False)
+    seq = DataParallelContraction(sc, overlap=not args.no_overlap, concurrent_bwd=False, allreduce="nccl")
     launches_timed = dp.launches
     for q in range(args.steps):
         b_, N_, A_, ne_, dB_, B_, dA_ = pool[q % POOL]
@@ -488,8 +490,9 @@ def run_ours(args):
                        "channels": K, "out": "+".join(f"{K}x{L}{'e' if L % 2 == 0 else 'o'}" for L in cfg.out_L),
                        "lmax_in": cfg.lmax_in, "correlation": cfg.correlation, "elements": cfg.n_elements,
                        "capacity_nodes": CAPACITY, "bins": n_bins, "global_batch": int(nodes_all / args.steps),
-                       "step_imbalance_max_over_mean": round(imbalance, 5), "dW_allreduce": ("NCCL, overlapped with dA"
-                                                                                              if world > 1 else None),
+                       "step_imbalance_max_over_mean": round(imbalance, 5), "dW_allreduce": ({"peer": "libsymcon NVLink peer-memory kernel (symmetric buffers), dA concurrent",
+                                                        "nccl": "NCCL on a communication stream"}[args.allreduce]
+                                                       if world > 1 else None),
                        "seq_len": None, "parallelism": f"dp{world}", "l2": "inputs > L2 (A 410 MB/bin), 4-bin pool",
                        "alg1_pack_s": round(t_pack, 3)},
             "per_gpu_nodes_per_s": value / world,

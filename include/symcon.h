@@ -179,6 +179,19 @@ symcon_status symcon_pack_balanced(const int64_t* sizes, int64_t n, int64_t capa
                                    int32_t workers, int64_t* bin_offsets, int64_t* graph_ids,
                                    int64_t max_bins, int64_t* n_bins);
 
+/* ---- dW all-reduce over NVLink peer memory ----------------
+ * bufs[r] (r < world <= 8): device pointer, valid on this GPU (peer mapping), of rank r's
+ * n-float partial; pads[r]: rank r's signal pad (>= world uint32 slots, zero-initialised, peer
+ * mapped). One kernel: a cross-GPU barrier (this rank writes `epoch` to slot `rank` of every pad,
+ * then waits until all slots of its own pad reach `epoch`; epochs must increase by call), then
+ * out[i] = sum_{r = 0..world-1} bufs[r][i] in rank order (bitwise identical on every rank).
+ * The caller must not overwrite bufs[rank] until every rank's call has completed (alternate two
+ * buffers per step). err (device int, may be NULL) is set to 1 if a peer did not arrive within
+ * ~seconds (the kernel then returns partial sums instead of hanging). out may alias bufs[rank]
+ * only if no peer reads it afterwards. */
+symcon_status symcon_peer_allreduce(const float* const* bufs, uint32_t* const* pads, int32_t world, int32_t rank,
+                                    int64_t n, uint32_t epoch, float* out, int32_t* err, void* stream);
+
 /* ---- channelwise tensor product + edge->node sum ----------------
  * Alg. 2 of the paper, the message construction that feeds the contraction,
  * with the neighbour sum of Eq. (1):

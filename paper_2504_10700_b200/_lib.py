@@ -25,7 +25,7 @@ EXPORTS = ["symcon_build_tables", "symcon_plan_info", "symcon_plan_path", "symco
            "symcon_pack_balanced", "symcon_precompile", "symcon_plan_source", "symcon_profile_enable",
            "symcon_profile_reset", "symcon_profile_read", "symcon_tp_build", "symcon_tp_info", "symcon_tp_path",
            "symcon_tp_workspace_bytes", "symcon_tp_forward", "symcon_tp_backward", "symcon_tp_check_device_error",
-           "symcon_tp_last_launch_count", "symcon_tp_source", "symcon_tp_destroy"]
+           "symcon_tp_last_launch_count", "symcon_tp_source", "symcon_tp_destroy", "symcon_peer_allreduce"]
 
 
 class SymconInfo(ctypes.Structure):
@@ -289,3 +289,15 @@ def symcon_tp_destroy(plan):
 
 def symcon_tp_last_launch_count(plan):
     return lib.symcon_tp_last_launch_count(plan)
+
+
+# ------------------------------------------------------------ dW all-reduce over peer memory
+lib.symcon_peer_allreduce.argtypes = [_vp, _vp, _i32, _i32, _i64, ctypes.c_uint32, _vp, _vp, _vp]
+lib.symcon_peer_allreduce.restype = ctypes.c_int
+
+
+def symcon_peer_allreduce(bufs, pads, rank, n, epoch, out, err, stream):
+    world = len(bufs)
+    b = (_vp * world)(*bufs)
+    p = (_vp * world)(*pads)
+    check(lib.symcon_peer_allreduce(b, p, world, rank, n, epoch, out, err, stream), "symcon_peer_allreduce")

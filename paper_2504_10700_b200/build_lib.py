@@ -16,7 +16,7 @@ CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-SOURCES = ["cg.cpp", "builder.cpp", "codegen.cpp", "pack.cpp", "api.cpp", "tp.cpp", "bucket.cu", "tp_static.cu"]
+SOURCES = ["cg.cpp", "builder.cpp", "codegen.cpp", "pack.cpp", "api.cpp", "tp.cpp", "bucket.cu", "tp_static.cu", "peer.cu"]
 
 # (lmax_in, correlation, out_L): BASELINE configs + the corr-1/2 cases the tests use
 PRESETS = [(3, 3, (0,)), (3, 3, (0, 1)), (3, 3, (0, 1, 2)), (3, 1, (0, 1, 2, 3)), (3, 2, (0,)),

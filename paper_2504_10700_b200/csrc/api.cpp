@@ -721,6 +721,32 @@ symcon_status symcon_backward2(const symcon_plan* p, int64_t N, const float* A, 
   return cuda_err(cudaGetLastError(), "backward2 launch");
 }
 
+symcon_status symcon_peer_allreduce(const float* const* bufs, uint32_t* const* pads, int32_t world, int32_t rank,
+                                    int64_t n, uint32_t epoch, float* out, int32_t* err, void* stream) {
+  if (!bufs || !pads || !out || world < 1 || world > 8 || rank < 0 || rank >= world || n < 0) {
+    set_error("bad peer all-reduce arguments");
+    return SYMCON_EINVAL;
+  }
+  PeerArgs a{};
+  for (int r = 0; r < world; r++) {
+    if (!bufs[r] || !pads[r]) { set_error("NULL peer pointer"); return SYMCON_EINVAL; }
+    a.buf[r] = bufs[r];
+    a.pad[r] = pads[r];
+  }
+  static int* dummy_err = nullptr;
+  if (!err) {
+    if (!dummy_err) cudaMalloc(&dummy_err, sizeof(int));
+    err = dummy_err;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long n4 = (n + 3) / 4;
+  const int blocks = (int)std::max<long long>(1, std::min<long long>(sms, (n4 + 511) / 512));
+  peer_allreduce_launch(a, world, rank, n, epoch, out, err, blocks, (cudaStream_t)stream);
+  return cuda_err(cudaGetLastError(), "peer all-reduce launch");
+}
+
 symcon_status symcon_check_device_error(const symcon_plan* p, void* ws, void* stream, int64_t* first_bad) {
   if (!p || !ws) { set_error("NULL argument"); return SYMCON_EINVAL; }
   cudaStream_t st = (cudaStream_t)stream;

@@ -30,6 +30,14 @@ size_t bucket_chunks(int64_t N);
 // stot[z][j][k] = sum over items it of element z (item order) of spart[it][j][k]
 int reduce_items_launch(const float* spart, const int* item_off, int E, int npad, int K, float* stot, cudaStream_t st);
 
+// dW all-reduce over peer memory (peer.cu)
+struct PeerArgs {
+  const float* buf[8];   // each rank's symmetric dW buffer (peer pointers)
+  unsigned* pad[8];      // each rank's signal pad (uint32 flags, slot r written by rank r)
+};
+int peer_allreduce_launch(const PeerArgs& a, int world, int rank, long long n, unsigned epoch, float* out, int* err,
+                          int blocks, cudaStream_t st);
+
 // channelwise TP (tp_static.cu)
 struct TPCsrArgs {
   const int* sender;

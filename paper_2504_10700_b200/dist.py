@@ -8,6 +8,10 @@
   backward dW, NCCL all-reduce of dW (the one cross-GPU exchange; PAPER.md:960 DDP all-reduce)
   on a communication stream, overlapped with the backward dA kernel. For force training the
   double backward's W_bar is all-reduced the same way, overlapped with its tile kernel.
+* allreduce="peer" (default for N > 1 when torch symmetric memory is available): dW is written
+  straight into a symmetric (peer-mapped) buffer and libsymcon's own kernel does the cross-GPU
+  barrier and the rank-ordered sum over NVLink P2P loads (symcon_peer_allreduce): no NCCL kernel
+  competing with the persistent dA grid, bitwise-identical dW on every rank.
 """
 import numpy as np
 import torch
@@ -44,15 +48,52 @@ class BinPackedShards:
         return np.add.reduceat(self.sizes[self.ids], self.offsets[:-1]) if self.n_bins else np.zeros(0)
 
 
+class PeerReducer:
+    """Two symmetric (peer-mapped) fp32 buffers used alternately per step + one signal pad; the
+    all-reduce itself is libsymcon's kernel (no NCCL)."""
+
+    def __init__(self, numel, device, group=None):
+        import torch.distributed._symmetric_memory as symm
+        grp = group if group is not None else dist.group.WORLD
+        try:
+            symm.enable_symm_mem_for_group(grp.group_name)
+        except Exception:  # noqa: BLE001  (newer torch: not needed)
+            pass
+        self.numel = int(numel)
+        self.bufs = [symm.empty(self.numel, dtype=torch.float32, device=device) for _ in range(2)]
+        self.hdl = [symm.rendezvous(b, grp) for b in self.bufs]
+        self.rank, self.world = self.hdl[0].rank, self.hdl[0].world_size
+        pad = self.hdl[0].get_signal_pad(self.rank, (self.world,), dtype=torch.int32)
+        pad.zero_()
+        self.err = torch.zeros(1, dtype=torch.int32, device=device)
+        torch.cuda.synchronize(device)
+        dist.barrier(group=group)
+        self.epoch = 0
+        self.parity = 0
+
+    def buffer(self):
+        return self.bufs[self.parity]
+
+    def allreduce(self, out, stream):
+        self.epoch += 1
+        h = self.hdl[self.parity]
+        _lib.symcon_peer_allreduce(list(h.buffer_ptrs), list(self.hdl[0].signal_pad_ptrs), self.rank, self.numel,
+                                   self.epoch, out.data_ptr(), self.err.data_ptr(), stream)
+        self.parity ^= 1
+        return out
+
+
 class DataParallelContraction:
     """Forward + backward of one rank's bin. The dW kernels run on the main stream and the dA
     kernel on a side stream (concurrently; `concurrent_bwd`), and for N > 1 the dW all-reduce
     runs on a communication stream as soon as dW is ready, overlapped with dA."""
 
-    def __init__(self, sc, group=None, overlap=True, concurrent_bwd=None):
+    def __init__(self, sc, group=None, overlap=True, concurrent_bwd=None, allreduce=None):
         self.sc = sc
         self.group = group
         self.overlap = overlap
+        self.allreduce = allreduce or "peer"
+        self._peer = None
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         # measured (profiles/r01): concurrent dW/dA helps at N=1 (+2-4%); at N=2/4 the sequential
         # dW -> (all-reduce || dA) order is erratic (the NCCL kernel becomes ready together with the
@@ -86,6 +127,22 @@ class DataParallelContraction:
             main.wait_stream(self.side)
             return dA, dW
         main = torch.cuda.current_stream(sc.device)
+        if self.allreduce == "peer":
+            if self._peer is None:
+                self._peer = PeerReducer(W.numel(), sc.device, self.group)
+            if dW is None:
+                dW = torch.empty_like(W)
+            self.side.wait_stream(main)
+            part = self._peer.buffer()[:W.numel()].view(W.shape)
+            sc.backward_raw(A, W, node_elem, dB, need_dA=False, dW=part, reuse=True)
+            self.launches += sc.last_launch_count()
+            with torch.cuda.stream(self.side):
+                dA, _ = sc.backward_raw(A, W, node_elem, dB, need_dW=False, dA=dA, reuse=True)
+                self.launches += sc.last_launch_count()
+            self._peer.allreduce(dW, main.cuda_stream)
+            self.launches += 1
+            main.wait_stream(self.side)
+            return dA, dW
         if not self.overlap:
             dA, dW = sc.backward_raw(A, W, node_elem, dB, dA=dA, dW=dW, reuse=True)
             self.launches += sc.last_launch_count()

@@ -1,0 +1,70 @@
+"""Multi-GPU (>= 2 devices, skipped otherwise): the NVLink peer-memory dW all-reduce
+(symcon_peer_allreduce via dist.PeerReducer) against NCCL's all-reduce, and bitwise agreement of
+the reduced dW across ranks."""
+import os
+import socket
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    torch.cuda.set_device(rank)
+    import torch.distributed as dist
+    dist.init_process_group("nccl", device_id=torch.device("cuda", rank))
+    from paper_2504_10700_b200.ops import SymmetricContraction
+    from paper_2504_10700_b200.dist import DataParallelContraction
+    from synth.inputs import gen_A, gen_W, gen_node_elem, gen_dB
+    sc = SymmetricContraction(3, 3, (0, 1), 17, 64, device=rank)
+    W = gen_W(17, sc.block_sizes(), 64, "cuda")
+    res = []
+    for step in range(3):   # several steps: both symmetric buffers and increasing epochs
+        N = 3000 + 500 * rank + 100 * step
+        A = gen_A(N, 64, 16, "cuda", seed=10 * step + rank)
+        ne = gen_node_elem(N, 17, "zipf", "cuda", seed=10 * step + rank)
+        dB = gen_dB(N, sc.out_dim, "cuda", seed=10 * step + rank)
+        dp = DataParallelContraction(sc, allreduce="peer") if step == 0 else dp
+        sc.forward_raw(A, W, ne)
+        dA, dW = dp.backward(A, W, ne, dB)
+        _, local = sc.backward_raw(A, W, ne, dB, need_dA=False)
+        ref = local.clone()
+        dist.all_reduce(ref)
+        torch.cuda.synchronize()
+        assert int(dp._peer.err.item()) == 0
+        err = (dW - ref).abs().max().item() / ref.abs().max().item()
+        allw = [torch.empty_like(dW) for _ in range(world)]
+        dist.all_gather(allw, dW)
+        same = all(torch.equal(allw[0], x) for x in allw)
+        res.append((err, same))
+    q.put((rank, res))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_peer_allreduce_matches_nccl_two_gpus():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(timeout=600)
+        assert p.exitcode == 0
+    out = [q.get() for _ in range(2)]
+    for rank, res in out:
+        for err, same in res:
+            assert err < 1e-6 and same, (rank, err, same)
