@@ -384,8 +384,10 @@ def run_ours(args):
         dist.all_gather(tt, t)
         ms_max = max(float(x[0]) for x in tt)
         nodes_all = sum(float(x[1]) for x in tt)
+        per_rank_ms = [round(float(x[0]) / args.steps, 4) for x in tt]
     else:
         ms_max, nodes_all = ms, float(nodes)
+        per_rank_ms = [round(ms / args.steps, 4)]
     value = nodes_all / (ms_max / 1e3)
 
     # ---- e2e through the public API with host buffers (pinned), copies inside the timed region
@@ -496,6 +498,7 @@ def run_ours(args):
                        "seq_len": None, "parallelism": f"dp{world}", "l2": "inputs > L2 (A 410 MB/bin), 4-bin pool",
                        "alg1_pack_s": round(t_pack, 3)},
             "per_gpu_nodes_per_s": value / world,
+            "per_rank_ms_per_step": per_rank_ms,
             "path_tops": path_ops / (ms_max / args.steps / 1e3) / 1e12,
             "path_frac_of_alu_peak": path_ops / (ms_max / args.steps / 1e3) / 1e12 / (148 * 128 * 1.965e-3),
             "path_roofline": path_roofline(cfg, sc, nodes / args.steps, path_ops, ms_max / args.steps, args.double_backward),
