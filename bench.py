@@ -176,6 +176,8 @@ class ClockSampler:
         self.t0 = self.t1 = None
 
     def __enter__(self):
+        if os.environ.get("BENCH_NO_CLOCKS"):
+            return self
         try:
             self._p = subprocess.Popen([sys.executable, "-c", _CLOCK_CHILD, str(self.index)], stdin=subprocess.PIPE,
                                        stdout=subprocess.PIPE, text=True)
