@@ -155,7 +155,7 @@ out = []
 while not select.select([sys.stdin], [], [], 0)[0]:
     out.append((time.time(), pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
                 pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
-    time.sleep(0.002)
+    time.sleep(float(sys.argv[2]))
 sys.stdin.readline()
 print(json.dumps(out), flush=True)
 """
@@ -179,7 +179,8 @@ class ClockSampler:
         if os.environ.get("BENCH_NO_CLOCKS"):
             return self
         try:
-            self._p = subprocess.Popen([sys.executable, "-c", _CLOCK_CHILD, str(self.index)], stdin=subprocess.PIPE,
+            period = float(os.environ.get("BENCH_CLOCK_MS", "10")) / 1e3
+            self._p = subprocess.Popen([sys.executable, "-c", _CLOCK_CHILD, str(self.index), str(period)], stdin=subprocess.PIPE,
                                        stdout=subprocess.PIPE, text=True)
             self.max_mhz = json.loads(self._p.stdout.readline())["ready"]
             time.sleep(0.02)
