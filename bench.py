@@ -178,6 +178,8 @@ class ClockSampler:
     def __enter__(self):
         if os.environ.get("BENCH_NO_CLOCKS"):
             return self
+        if os.environ.get("BENCH_CLOCK_RANK0") and int(os.environ.get("LOCAL_RANK", "0")) != 0:
+            return self
         try:
             period = float(os.environ.get("BENCH_CLOCK_MS", "10")) / 1e3
             self._p = subprocess.Popen([sys.executable, "-c", _CLOCK_CHILD, str(self.index), str(period)], stdin=subprocess.PIPE,
