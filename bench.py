@@ -358,6 +358,11 @@ def run_ours(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     nodes = 0
     with ClockSampler(local) as clk:
+        # ranks enter the timed region together (the sampler start-up takes a variable fraction
+        # of a second per rank; without this barrier the first rank's wait is charged to the others)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
         clk.start()
         e0.record()
         for q in range(args.steps):
@@ -592,6 +597,11 @@ def run_tp(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     nodes = edges = 0
     with ClockSampler(local) as clk:
+        # ranks enter the timed region together (the sampler start-up takes a variable fraction
+        # of a second per rank; without this barrier the first rank's wait is charged to the others)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
         clk.start()
         e0.record()
         for q in range(args.steps):
