@@ -95,10 +95,8 @@ class DataParallelContraction:
         self.allreduce = allreduce or "peer"
         self._peer = None
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
-        # measured (profiles/r01): concurrent dW/dA helps at N=1 (+2-4%); at N=2/4 the sequential
-        # dW -> (all-reduce || dA) order is erratic (the NCCL kernel becomes ready together with the
-        # persistent dA grid and waits for SMs while its peers spin: 1.3-4.6 ms per step), while dA
-        # started together with dW leaves the all-reduce to run as SMs free up: stable 1.30 ms at N=2
+        # measured (profiles/r01): dA concurrent with dW helps at N=1 (+2-4%) and is the default at
+        # every N (the dW all-reduce then runs as SMs free up)
         self.concurrent_bwd = True if concurrent_bwd is None else concurrent_bwd
         self.side = torch.cuda.Stream(device=sc.device) if self.concurrent_bwd else None
         self.comm = torch.cuda.Stream(device=sc.device) if self.world > 1 else None
