@@ -178,6 +178,24 @@ class DataParallelContraction:
             self.launches += sc.last_launch_count()
             return out
         main = torch.cuda.current_stream(sc.device)
+        if self.allreduce == "peer":
+            if getattr(self, "_peer2", None) is None:
+                self._peer2 = PeerReducer(W.numel(), sc.device, self.group)
+            part = self._peer2.buffer()[:W.numel()].view(W.shape)
+            self.side.wait_stream(main)
+            # W_bar partial straight into the symmetric buffer (main), the tile part on the side stream
+            sc.backward2_raw(A, W, node_elem, dB, uA, False, False, True, reuse=True, W_bar=part)
+            self.launches += sc.last_launch_count()
+            dBb = Ab = None
+            if need_dB or need_A:
+                with torch.cuda.stream(self.side):
+                    dBb, Ab, _ = sc.backward2_raw(A, W, node_elem, dB, uA, need_dB, need_A, False, reuse=True)
+                    self.launches += sc.last_launch_count()
+            Wb = torch.empty_like(W)
+            self._peer2.allreduce(Wb, main.cuda_stream)
+            self.launches += 1
+            main.wait_stream(self.side)
+            return dBb, Ab, Wb
         _, _, Wb = sc.backward2_raw(A, W, node_elem, dB, uA, False, False, True, reuse=True)
         self.launches += sc.last_launch_count()
         self.comm.wait_stream(main)

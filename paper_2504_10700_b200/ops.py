@@ -98,14 +98,15 @@ class SymmetricContraction:
         return (dA if need_dA else None), (dW if need_dW else None)
 
     def backward2_raw(self, A, W, node_elem, dB, uA, need_dB=True, need_A=True, need_W=True, ws_key="default",
-                      reuse=False):
-        """Double backward: (dB_bar, A_bar, W_bar) = derivatives of <uA, dA(A, W, dB)> (symcon_backward2)."""
+                      reuse=False, W_bar=None):
+        """Double backward: (dB_bar, A_bar, W_bar) = derivatives of <uA, dA(A, W, dB)> (symcon_backward2).
+        W_bar may be given (e.g. a symmetric buffer for the peer all-reduce)."""
         N = self._check(A, W, node_elem)
         assert dB.dtype == torch.float32 and dB.is_contiguous() and dB.shape == (N, self.out_dim)
         assert uA.dtype == torch.float32 and uA.is_contiguous() and uA.shape == A.shape
         dBb = torch.empty_like(dB) if need_dB else None
         Ab = torch.empty_like(A) if need_A else None
-        Wb = torch.empty_like(W) if need_W else None
+        Wb = (W_bar if W_bar is not None else torch.empty_like(W)) if need_W else None
         ws = self.workspace(N, ws_key)
         flags = (_lib.SYMCON_REUSE_BUCKETS | _lib.SYMCON_REUSE_FOLD) if reuse else 0
         ptr = lambda x: x.data_ptr() if x is not None else None

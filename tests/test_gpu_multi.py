@@ -46,7 +46,13 @@ def _worker(rank, world, port, q):
         allw = [torch.empty_like(dW) for _ in range(world)]
         dist.all_gather(allw, dW)
         same = all(torch.equal(allw[0], x) for x in allw)
-        res.append((err, same))
+        uA = gen_A(N, 64, 16, "cuda", seed=77 + step)
+        _, _, Wb = dp.backward2(A, W, ne, dB, uA)
+        _, _, Wl = sc.backward2_raw(A, W, ne, dB, uA, False, False, True)
+        dist.all_reduce(Wl)
+        torch.cuda.synchronize()
+        err2 = (Wb - Wl).abs().max().item() / Wl.abs().max().item()
+        res.append((max(err, err2), same))
     q.put((rank, res))
     dist.barrier()
     dist.destroy_process_group()
