@@ -1,0 +1,45 @@
+"""bench.py's work accounting (CPU): the per-(node, channel) op counts and HBM bytes the roofline
+fields are computed from."""
+import os
+import sys
+
+import pytest
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2504_10700_b200 import build_lib
+    build_lib.build()
+    from paper_2504_10700_b200 import _lib
+    return _lib
+
+
+def test_alg_ops_matches_design_counts(L):
+    import bench
+
+    class S:
+        pass
+    sc = S()
+    sc.plan = L.symcon_build_tables(3, 3, [0, 1], 89, 128, -1)
+    ops = bench.alg_ops(sc)
+    # DESIGN.md §7 table (MP-medium)
+    assert (ops["fwd"], ops["dA"], ops["dW"], ops["path"], ops["bwd2"], ops["bwd2_dW"]) == (888, 1486, 888, 3146, 3431, 1482)
+    assert ops["n_fold"] == 410 and ops["prefixes"] == 123 and ops["deg3_monomials"] == 355
+    L.symcon_destroy(sc.plan)
+
+
+def test_tp_bytes_and_path_roofline():
+    import bench
+    from synth.inputs import CONFIGS
+    f, b = bench.tp_bytes(50_000, 1_500_000, 128, 10, 4, 16, 16)
+    # R (E K P floats) dominates: 7.68 GB read in the forward, read + written (dR) in the backward
+    assert f == 4 * (1_500_000 * 128 * 10 + 50_000 * 128 * 4 + 1_500_000 * 16 + 50_000 * 128 * 16) + 8 * 1_500_000
+    assert b - f == 4 * (1_500_000 * 16 + 50_000 * 128 * 4 + 1_500_000 * 128 * 10)
+
+    class S:
+        out_dim = 128 * 4
+    r = bench.path_roofline(CONFIGS["mp_medium"], S(), 50_000, 3146 * 50_000 * 128, 1.2, False)
+    assert r["bytes_per_node_channel"] == 224 and r["bound"] == "alu"
+    assert abs(r["t_alu_ms"] - 3146 * 50_000 * 128 / (148 * 128 * 1.965e9) * 1e3) < 1e-9
