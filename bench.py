@@ -216,7 +216,7 @@ class ClockSampler:
         sm = [m for m, _ in win]
         reasons = sorted({name for _, r in win for name, bit in self.REASONS.items() if r & bit})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_min_mhz": min(sm) if sm else None,
-                "sm_max_mhz": mx, "reasons": reasons, "samples": len(sm), "source": "nvml ~2ms (sampler process)"}
+                "sm_max_mhz": mx, "reasons": reasons, "samples": len(sm), "source": f"nvml every {os.environ.get('BENCH_CLOCK_MS', '10')} ms (sampler process)"}
 
 
 # ----------------------------------------------------------------------------- cpu oracle
