@@ -70,7 +70,7 @@ struct KernelConfig {
                                    // room for concurrent dW CTAs on the same SMs
   int dw2_rows_per_group = 0;      // double-backward W_bar kernel (same layout): rows per warp; 0 = auto
   int dw2_groups_per_cta = 0;      // double-backward W_bar kernel: warps per CTA; 0 = auto
-  bool dw_qform = false;           // transposed dW: q = dB_o p_ab products shared by the prefix's rows
+  int dw_qform = -1;               // transposed dW: q = dB_o p_ab products shared by the prefix's rows; -1 auto
   int dw_np_unroll = 1;            // transposed dW: unroll of the node-pair loop (software pipelining)
   int dw_batch = 1;                // transposed dW: rows whose products are emitted before their FMAs
   int dw_block_nodes = 8;          // transposed dW: nodes per smem stage
