@@ -218,6 +218,9 @@ typedef struct symcon_tp_plan symcon_tp_plan; /* opaque */
  * channels K >= 1. device < 0: host-only plan (tables and source, no kernels). */
 symcon_status symcon_tp_build(int lmax_y, const int* hidden_l, int n_hidden, int lmax_out, int channels,
                               int device, symcon_tp_plan** plan);
+/* Build-host helper (no device needed): NVRTC-compile a TP configuration's kernels (they depend
+ * on K) into the cubin cache. */
+symcon_status symcon_tp_precompile(int lmax_y, const int* hidden_l, int n_hidden, int lmax_out, int channels);
 /* n_paths, n_y = (lmax_y+1)^2, n_h, n_out = (lmax_out+1)^2 */
 symcon_status symcon_tp_info(const symcon_tp_plan* plan, int32_t* n_paths, int32_t* n_y, int32_t* n_h,
                              int32_t* n_out);

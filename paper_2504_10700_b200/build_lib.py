@@ -61,6 +61,21 @@ def build(verbose=False):
     return OUT
 
 
+# channelwise TP (lmax_y, hidden_l, lmax_out, K): the bench shape and the test configurations
+TP_PRESETS = [(3, (0, 1), 3, 128), (3, (0, 1), 3, 64), (3, (0, 1), 3, 32), (3, (0, 1), 3, 6), (3, (0,), 3, 64),
+              (3, (0, 1, 2), 3, 32), (2, (0, 1), 2, 13), (2, (0, 1), 2, 96), (1, (1,), 1, 40), (3, (0, 1, 2, 3), 3, 33)]
+
+
+def precompile_tp(presets=TP_PRESETS):
+    lib = ctypes.CDLL(build())
+    lib.symcon_tp_precompile.restype = ctypes.c_int
+    lib.symcon_last_error.restype = ctypes.c_char_p
+    for ly, hid, lo, k in presets:
+        arr = (ctypes.c_int * len(hid))(*hid)
+        if lib.symcon_tp_precompile(ly, arr, len(hid), lo, k) != 0:
+            raise RuntimeError(f"tp precompile {ly},{hid},{lo},{k} failed: {lib.symcon_last_error().decode()}")
+
+
 def precompile(presets=PRESETS):
     lib = ctypes.CDLL(build())
     lib.symcon_precompile.restype = ctypes.c_int
