@@ -40,6 +40,7 @@ struct symcon_plan {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t k_fold = nullptr, k_fwd = nullptr, k_dA = nullptr, k_dW = nullptr, k_unfold = nullptr;
   cudaKernel_t k_bwd2 = nullptr, k_bwd2_dW = nullptr;
+  cudaKernel_t k_fwd_g = nullptr, k_dA_g = nullptr;   // gamma variants (kc.gamma)
   mutable std::atomic<int> last_launches{0};
   // optional launch timer (symcon_profile_*): CUDA events around each launch group
   struct Rec { int kind; cudaEvent_t a, b; };
@@ -308,6 +309,7 @@ static symcon_status build_common(int lmax_in, int corr, const int* out_L, int n
   if (p->kc.dw_groups_per_cta <= 0) p->kc.dw_groups_per_cta = 8;
   // q-form dW measured 6% faster at 9 outputs per channel (large), 1.5% slower at 4 (MP-medium)
   if (p->kc.dw_qform < 0) p->kc.dw_qform = p->t.out_per_ch > 4 ? 1 : 0;
+  if (p->kc.gamma < 0) p->kc.gamma = p->t.rows.size() <= 128 ? 1 : 0;
   // W_bar also holds the JVP direction rows in registers: at most 8 warps (255 registers each)
   // (and enough warps that the register staging of A, U and dB stays small)
   if (p->kc.dw2_rows_per_group <= 0) {
@@ -354,6 +356,8 @@ symcon_status symcon_build_tables(int lmax_in, int correlation, const int* out_L
     if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_unfold, p->lib, "symcon_unfold"), "get symcon_unfold");
     if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_bwd2, p->lib, "symcon_bwd2"), "get symcon_bwd2");
     if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_bwd2_dW, p->lib, "symcon_bwd2_dW"), "get symcon_bwd2_dW");
+    if (!s && p->kc.gamma > 0) s = cuda_err(cudaLibraryGetKernel(&p->k_fwd_g, p->lib, "symcon_fwd_g"), "get symcon_fwd_g");
+    if (!s && p->kc.gamma > 0) s = cuda_err(cudaLibraryGetKernel(&p->k_dA_g, p->lib, "symcon_bwd_dA_g"), "get symcon_bwd_dA_g");
     p->tile_smem = sizeof(float) * (size_t)p->kc.tile_warps * (2 * (size_t)p->npad) + 16 * (size_t)p->kc.tile_warps;
     if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                          (int)p->tile_smem, device), "fwd smem attribute");
@@ -592,8 +596,12 @@ symcon_status symcon_forward(const symcon_plan* p, int64_t N, const float* A, co
   void* args[] = {&q};
   {
     Timed tm(p, K_FWD, st);
-    s = cuda_err(cudaLaunchKernel((const void*)p->k_fwd, dim3(p->grid_fwd), dim3(32 * p->kc.tile_warps), args, p->tile_smem, st),
-                 "launch symcon_fwd");
+    if (p->k_fwd_g)
+      s = cuda_err(cudaLaunchKernel((const void*)p->k_fwd_g, dim3((unsigned)((w.max_tiles + 3) / 4), (p->t.K + 31) / 32), dim3(128),
+                                    args, 0, st), "launch symcon_fwd_g");
+    else
+      s = cuda_err(cudaLaunchKernel((const void*)p->k_fwd, dim3(p->grid_fwd), dim3(32 * p->kc.tile_warps), args, p->tile_smem, st),
+                   "launch symcon_fwd");
   }
   n++;
   if (s) return s;
@@ -652,8 +660,12 @@ symcon_status symcon_backward_ex(const symcon_plan* p, int64_t N, const float* A
   if (dA) {
     {
     Timed tm(p, K_DA, st);
-    s = cuda_err(cudaLaunchKernel((const void*)p->k_dA, dim3(p->grid_dA), dim3(32 * p->kc.tile_warps), args, p->tile_smem, st),
-                 "launch symcon_bwd_dA");
+    if (p->k_dA_g)
+      s = cuda_err(cudaLaunchKernel((const void*)p->k_dA_g, dim3((unsigned)((w.max_tiles + 3) / 4), (p->t.K + 31) / 32), dim3(128),
+                                    args, 0, st), "launch symcon_bwd_dA_g");
+    else
+      s = cuda_err(cudaLaunchKernel((const void*)p->k_dA, dim3(p->grid_dA), dim3(32 * p->kc.tile_warps), args, p->tile_smem, st),
+                   "launch symcon_bwd_dA");
     }
     if (s) return s;
     n++;
