@@ -309,7 +309,9 @@ static symcon_status build_common(int lmax_in, int corr, const int* out_L, int n
   if (p->kc.dw_groups_per_cta <= 0) p->kc.dw_groups_per_cta = 8;
   // q-form dW measured 6% faster at 9 outputs per channel (large), 1.5% slower at 4 (MP-medium)
   if (p->kc.dw_qform < 0) p->kc.dw_qform = p->t.out_per_ch > 4 ? 1 : 0;
-  if (p->kc.gamma < 0) p->kc.gamma = p->t.rows.size() <= 128 ? 1 : 0;
+  // gamma kernels (bit 1: forward, bit 2: dA): measured on the OFF-small shape, the gamma dA is
+  // 16% faster than the persistent one and the gamma forward 27% slower -> auto = dA only
+  if (p->kc.gamma < 0) p->kc.gamma = p->t.rows.size() <= 128 ? 2 : 0;
   // W_bar also holds the JVP direction rows in registers: at most 8 warps (255 registers each)
   // (and enough warps that the register staging of A, U and dB stays small)
   if (p->kc.dw2_rows_per_group <= 0) {
@@ -356,8 +358,8 @@ symcon_status symcon_build_tables(int lmax_in, int correlation, const int* out_L
     if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_unfold, p->lib, "symcon_unfold"), "get symcon_unfold");
     if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_bwd2, p->lib, "symcon_bwd2"), "get symcon_bwd2");
     if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_bwd2_dW, p->lib, "symcon_bwd2_dW"), "get symcon_bwd2_dW");
-    if (!s && p->kc.gamma > 0) s = cuda_err(cudaLibraryGetKernel(&p->k_fwd_g, p->lib, "symcon_fwd_g"), "get symcon_fwd_g");
-    if (!s && p->kc.gamma > 0) s = cuda_err(cudaLibraryGetKernel(&p->k_dA_g, p->lib, "symcon_bwd_dA_g"), "get symcon_bwd_dA_g");
+    if (!s && (p->kc.gamma & 1)) s = cuda_err(cudaLibraryGetKernel(&p->k_fwd_g, p->lib, "symcon_fwd_g"), "get symcon_fwd_g");
+    if (!s && (p->kc.gamma & 2)) s = cuda_err(cudaLibraryGetKernel(&p->k_dA_g, p->lib, "symcon_bwd_dA_g"), "get symcon_bwd_dA_g");
     p->tile_smem = sizeof(float) * (size_t)p->kc.tile_warps * (2 * (size_t)p->npad) + 16 * (size_t)p->kc.tile_warps;
     if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                          (int)p->tile_smem, device), "fwd smem attribute");

@@ -70,8 +70,8 @@ struct KernelConfig {
                                    // room for concurrent dW CTAs on the same SMs
   int dw2_rows_per_group = 0;      // double-backward W_bar kernel (same layout): rows per warp; 0 = auto
   int dw2_groups_per_cta = 0;      // double-backward W_bar kernel: warps per CTA; 0 = auto
-  int gamma = -1;                  // fwd/dA with lane = channel and register-resident coefficients
-                                   // (few folded rows, HBM-bound shapes); -1 auto (rows <= 128)
+  int gamma = -1;                  // fwd (bit 1) / dA (bit 2) with lane = channel and register-resident
+                                   // coefficients (few folded rows); -1 auto (dA only, rows <= 128)
   int dw_qform = -1;               // transposed dW: q = dB_o p_ab products shared by the prefix's rows; -1 auto
   int dw_np_unroll = 1;            // transposed dW: unroll of the node-pair loop (software pipelining)
   int dw_batch = 1;                // transposed dW: rows whose products are emitted before their FMAs
