@@ -261,8 +261,39 @@ class _TPFn(torch.autograd.Function):
         return tp.forward_raw(Y, h, R, sender, receiver)
 
     @staticmethod
-    @torch.autograd.function.once_differentiable
     def backward(ctx, dA):
         Y, h, R, sender, receiver = ctx.saved_tensors
+        if torch.is_grad_enabled():
+            # create_graph=True (forces in the loss flow through Y and R): differentiable backward
+            dY, dh, dR = _TPBwdFn.apply(Y, h, R, sender, receiver, dA.contiguous(), ctx.tp)
+            return dY, dh, dR, None, None, None
         dY, dh, dR = ctx.tp.backward_raw(Y, h, R, sender, receiver, dA.contiguous(), *ctx.needs_input_grad[:3])
         return dY, dh, dR, None, None, None
+
+
+class _TPBwdFn(torch.autograd.Function):
+    """(Y, h, R, dA) -> (dY, dh, dR) with its own backward. The TP is linear in each of Y, h, R,
+    so the second derivatives are TP passes with one input replaced by its cotangent:
+      dA_bar = TP(uY, h, R) + TP(Y, uh, R) + TP(Y, h, uR)
+      Y_bar  = dY|_(h := uh) + dY|_(R := uR),  h_bar = dh|_(Y := uY) + dh|_(R := uR),
+      R_bar  = dR|_(Y := uY) + dR|_(h := uh)   (all with the same dA)."""
+
+    @staticmethod
+    def forward(ctx, Y, h, R, sender, receiver, dA, tp):
+        ctx.tp = tp
+        ctx.save_for_backward(Y, h, R, sender, receiver, dA)
+        return tp.backward_raw(Y, h, R, sender, receiver, dA)
+
+    @staticmethod
+    @torch.autograd.function.once_differentiable
+    def backward(ctx, uY, uh, uR):
+        Y, h, R, s, r, dA = ctx.saved_tensors
+        tp = ctx.tp
+        z = lambda x, ref: torch.zeros_like(ref) if x is None else x.contiguous()
+        uY, uh, uR = z(uY, Y), z(uh, h), z(uR, R)
+        dA_bar = tp.forward_raw(uY, h, R, s, r)
+        dA_bar.add_(tp.forward_raw(Y, uh, R, s, r)).add_(tp.forward_raw(Y, h, uR, s, r))
+        a_Y, _, a_R = tp.backward_raw(Y, uh, R, s, r, dA, True, False, True)    # h := uh
+        b_Y, b_h, _ = tp.backward_raw(Y, h, uR, s, r, dA, True, True, False)    # R := uR
+        _, c_h, c_R = tp.backward_raw(uY, h, R, s, r, dA, False, True, True)    # Y := uY
+        return a_Y.add_(b_Y), b_h.add_(c_h), a_R.add_(c_R), None, None, dA_bar, None

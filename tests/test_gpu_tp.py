@@ -169,3 +169,27 @@ def test_tp_full_size_sampled():
     hY, hR = _host(Y[te], R[te])
     _, rh, _ = backward(prob, hY, hh, hR, hs[eidx], hr[eidx], N, hdA)
     assert _rel(dh[torch.from_numpy(nodes).cuda()].cpu(), rh[nodes]) < TOL
+
+
+def test_tp_double_backward_force_style_loss():
+    """create_graph=True through the TP (forces flow through Y and R): loss = <dY, V1> + <dh, V2> +
+    <dR, V3> of the gradients of <A, Rb>; its gradients against the oracle composition (pinned by
+    finite differences in tests/test_oracle_tp.py)."""
+    from oracle.tp import TPProblem, forward, backward
+    tp, Y, h, R, s, r, N = _setup(3, (0, 1), 3, 64, [20, 31], seed=4)
+    g = torch.Generator("cuda").manual_seed(6)
+    Rb = torch.randn((N, 64, tp.n_out), generator=g, device="cuda")
+    V1, V2, V3 = (torch.randn(x.shape, generator=g, device="cuda") for x in (Y, h, R))
+    Yg, hg, Rg, Rbg = (x.clone().requires_grad_(True) for x in (Y, h, R, Rb))
+    A = tp(Yg, hg, Rg, s, r)
+    gY, gh, gR = torch.autograd.grad((A * Rbg).sum(), (Yg, hg, Rg), create_graph=True)
+    ((gY * V1).sum() + (gh * V2).sum() + (gR * V3).sum()).backward()
+    torch.cuda.synchronize()
+    prob = TPProblem(3, (0, 1), 3)
+    hY, hh, hR, hs, hr, hRb, u1, u2, u3 = _host(Y, h, R, s, r, Rb, V1, V2, V3)
+    dA_bar = forward(prob, u1, hh, hR, hs, hr, N) + forward(prob, hY, u2, hR, hs, hr, N) + forward(prob, hY, hh, u3, hs, hr, N)
+    aY, _, aR = backward(prob, hY, u2, hR, hs, hr, N, hRb)
+    bY, bh, _ = backward(prob, hY, hh, u3, hs, hr, N, hRb)
+    _, ch, cR = backward(prob, u1, hh, hR, hs, hr, N, hRb)
+    for got, ref in ((Yg.grad, aY + bY), (hg.grad, bh + ch), (Rg.grad, aR + cR), (Rbg.grad, dA_bar)):
+        assert _rel(got.cpu(), ref) < TOL

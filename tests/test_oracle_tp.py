@@ -155,3 +155,33 @@ def test_backward_finite_differences_and_euler_identities():
             ap, am = [Y, h, R], [Y, h, R]
             ap[i], am[i] = Xp, Xm
             assert (f(*ap) - f(*am)) / (2 * eps) == pytest.approx(G[idx], rel=1e-7, abs=1e-7)
+
+
+def test_double_backward_composition_by_finite_differences():
+    """The TP is linear in each of Y, h, R, so the derivatives of <(uY, uh, uR), backward(Y, h, R, dA)>
+    are TP passes with one input replaced by its cotangent (ops._TPBwdFn): pinned here against
+    central differences of the oracle backward."""
+    prob = TPProblem(2, (0, 1), 2)
+    N, E, K = 5, 12, 2
+    Y, h, R, s, t, _, rng = _inputs(prob, N, E, K, seed=8, unit_y=False)
+    dA = rng.normal(size=(N, K, prob.n_out))
+    uY, uh, uR = rng.normal(size=Y.shape), rng.normal(size=h.shape), rng.normal(size=R.shape)
+
+    def L(Y_, h_, R_, dA_):
+        gY, gh, gR = backward(prob, Y_, h_, R_, s, t, N, dA_)
+        return (uY * gY).sum() + (uh * gh).sum() + (uR * gR).sum()
+
+    dA_bar = forward(prob, uY, h, R, s, t, N) + forward(prob, Y, uh, R, s, t, N) + forward(prob, Y, h, uR, s, t, N)
+    aY, _, aR = backward(prob, Y, uh, R, s, t, N, dA)
+    bY, bh, _ = backward(prob, Y, h, uR, s, t, N, dA)
+    _, ch, cR = backward(prob, uY, h, R, s, t, N, dA)
+    comp = {0: aY + bY, 1: bh + ch, 2: aR + cR, 3: dA_bar}
+    eps = 1e-6
+    args = [Y, h, R, dA]
+    for i in range(4):
+        for _ in range(3):
+            idx = tuple(rng.integers(0, n) for n in args[i].shape)
+            ap, am = [a.copy() for a in args], [a.copy() for a in args]
+            ap[i][idx] += eps
+            am[i][idx] -= eps
+            assert (L(*ap) - L(*am)) / (2 * eps) == pytest.approx(comp[i][idx], rel=1e-6, abs=1e-6)
