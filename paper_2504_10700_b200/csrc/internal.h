@@ -70,6 +70,7 @@ struct KernelConfig {
                                    // room for concurrent dW CTAs on the same SMs
   int dw2_rows_per_group = 0;      // double-backward W_bar kernel (same layout): rows per warp; 0 = auto
   int dw2_groups_per_cta = 0;      // double-backward W_bar kernel: warps per CTA; 0 = auto
+  int da_group = 0;                // dA: emit each prefix group's g first, then its D_c updates (operand reuse)
   int gamma = -1;                  // fwd (bit 1) / dA (bit 2) with lane = channel and register-resident
                                    // coefficients (few folded rows); -1 auto (dA only, rows <= 128)
   int dw_qform = -1;               // transposed dW: q = dB_o p_ab products shared by the prefix's rows; -1 auto
