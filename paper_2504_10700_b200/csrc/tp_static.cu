@@ -202,7 +202,7 @@ int tp_csr_launch(const TPCsrArgs& a, cudaStream_t st) {
     n++;
     if (a.E > 0) {
       tp_send_scatter<<<grid_for(a.E, 256), 256, 0, st>>>(a.sender, a.N, a.E, a.send_cur, a.send_perm);
-      tp_seg_sort_warp<<<grid_for((long long)a.N * 32, 256), 256, 0, st>>>(a.send_off, a.N, a.send_perm);
+      tp_seg_sort<<<grid_for(a.N, 128), 128, 0, st>>>(a.send_off, a.N, a.send_perm);  // (warp bitonic measured slower)
       tp_inv_perm<<<grid_for(a.E, 256), 256, 0, st>>>(a.send_perm, a.E, a.send_pos);
       n += 3;
     }
