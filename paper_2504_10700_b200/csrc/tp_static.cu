@@ -83,37 +83,7 @@ __global__ void tp_send_scatter(const int* __restrict__ sender, int N, int E, in
   }
 }
 
-// each sender's edge list sorted by edge id (deterministic order for the dh reduction): one warp
-// per sender; segments of up to 32 edges are sorted in registers by a bitonic network over the
-// lanes, longer ones by insertion sort in lane 0
-__global__ void tp_seg_sort_warp(const int* __restrict__ off, int N, int* __restrict__ perm) {
-  const int lane = threadIdx.x & 31;
-  for (int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < N; j += (gridDim.x * blockDim.x) >> 5) {
-    const int a = off[j], n = off[j + 1] - a;
-    if (n <= 1) continue;
-    if (n <= 32) {
-      int v = lane < n ? perm[a + lane] : 0x7fffffff;
-#pragma unroll
-      for (int k = 2; k <= 32; k <<= 1)
-#pragma unroll
-        for (int d = k >> 1; d > 0; d >>= 1) {
-          const int o = __shfl_xor_sync(0xffffffffu, v, d);
-          const bool up = ((lane & k) == 0);
-          const bool lower = ((lane & d) == 0);
-          v = (lower == up) ? min(v, o) : max(v, o);
-        }
-      if (lane < n) perm[a + lane] = v;
-    } else if (lane == 0) {
-      for (int q = a + 1; q < a + n; q++) {
-        const int v = perm[q];
-        int t = q - 1;
-        while (t >= a && perm[t] > v) { perm[t + 1] = perm[t]; t--; }
-        perm[t + 1] = v;
-      }
-    }
-  }
-}
-
+// each sender's edge list sorted by edge id (deterministic order for the dh reduction)
 __global__ void tp_seg_sort(const int* __restrict__ off, int N, int* __restrict__ perm) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
     const int a = off[j], b = off[j + 1];
