@@ -125,9 +125,14 @@ class DataParallelContraction:
             main.wait_stream(self.side)
             return dA, dW
         main = torch.cuda.current_stream(sc.device)
-        if self.allreduce == "peer":
-            if self._peer is None:
+        if self.allreduce == "peer" and self._peer is None:
+            try:
                 self._peer = PeerReducer(W.numel(), sc.device, self.group)
+            except Exception as exc:  # noqa: BLE001  (no symmetric memory on this system: NCCL)
+                import sys
+                print(f"[symcon] peer-memory all-reduce unavailable ({exc!r}); using NCCL", file=sys.stderr)
+                self.allreduce = "nccl"
+        if self.allreduce == "peer":
             if dW is None:
                 dW = torch.empty_like(W)
             self.side.wait_stream(main)
@@ -178,9 +183,14 @@ class DataParallelContraction:
             self.launches += sc.last_launch_count()
             return out
         main = torch.cuda.current_stream(sc.device)
-        if self.allreduce == "peer":
-            if getattr(self, "_peer2", None) is None:
+        if self.allreduce == "peer" and getattr(self, "_peer2", None) is None:
+            try:
                 self._peer2 = PeerReducer(W.numel(), sc.device, self.group)
+            except Exception as exc:  # noqa: BLE001
+                import sys
+                print(f"[symcon] peer-memory all-reduce unavailable ({exc!r}); using NCCL", file=sys.stderr)
+                self.allreduce = "nccl"
+        if self.allreduce == "peer":
             part = self._peer2.buffer()[:W.numel()].view(W.shape)
             self.side.wait_stream(main)
             # W_bar partial straight into the symmetric buffer (main), the tile part on the side stream
