@@ -520,7 +520,7 @@ def run_ours(args):
                        "lmax_in": cfg.lmax_in, "correlation": cfg.correlation, "elements": cfg.n_elements,
                        "capacity_nodes": CAPACITY, "bins": n_bins, "global_batch": int(nodes_all / args.steps),
                        "step_imbalance_max_over_mean": round(imbalance, 5), "dW_allreduce": ({"peer": "libsymcon NVLink peer-memory kernel (symmetric buffers), dA concurrent",
-                                                        "nccl": "NCCL on a communication stream"}[args.allreduce]
+                                                        "nccl": "NCCL on a communication stream"}[dp.allreduce]
                                                        if world > 1 else None),
                        "seq_len": None, "parallelism": f"dp{world}", "l2": "inputs > L2 (A 410 MB/bin), 4-bin pool",
                        "alg1_pack_s": round(t_pack, 3)},
