@@ -350,6 +350,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     s, bad = sc.check_device_error()
     assert s == 0, (s, bad)
+    if getattr(dp, "_peer", None) is not None:
+        assert int(dp._peer.err.item()) == 0, "peer all-reduce barrier timed out"
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -372,6 +374,8 @@ def run_ours(args):
         clk.end()
     if world > 1:
         dist.barrier()
+    if getattr(dp, "_peer", None) is not None:
+        assert int(dp._peer.err.item()) == 0, "peer all-reduce barrier timed out"
     ms = e0.elapsed_time(e1)
     # per-kernel times for the roofline: a separate pass with the kernels back to back on one
     # stream (the throughput region above overlaps dW and dA, which would blur each kernel's time)
