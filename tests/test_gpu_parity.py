@@ -70,6 +70,11 @@ def test_tiny_against_python_oracle():
     ("corr1_all_L", 3, 1, (0, 1, 2, 3), 3, 16, 300, "uniform"),
     ("corr2", 3, 2, (0, 1), 3, 16, 300, "uniform"),
     ("out_1o_only", 3, 3, (1,), 7, 32, 500, "zipf"),
+    ("scalars_only_lmax0", 0, 3, (0,), 3, 16, 300, "uniform"),
+    ("single_channel_element", 3, 3, (0, 1), 1, 1, 200, "uniform"),
+    ("odd_K255", 3, 3, (0,), 4, 255, 300, "uniform"),
+    ("out_2e_3o_corr2", 3, 2, (2, 3), 3, 24, 300, "uniform"),
+    ("out_0123_corr3", 2, 3, (0, 1, 2, 3), 3, 8, 200, "uniform"),
 ])
 def test_against_c_oracle(name, lmax, corr, outs, E, K, N, dist):
     from oracle.contraction import Problem
@@ -323,6 +328,9 @@ def test_backward2_tiny_against_python_oracle():
     ("corr1_all_L", 3, 1, (0, 1, 2, 3), 3, 16, 300, "uniform"),
     ("corr2", 3, 2, (0, 1), 3, 16, 300, "uniform"),
     ("out_1o_only", 3, 3, (1,), 7, 32, 500, "zipf"),
+    ("scalars_only_lmax0", 0, 3, (0,), 3, 16, 300, "uniform"),
+    ("odd_K255", 3, 3, (0,), 4, 255, 200, "uniform"),
+    ("out_2e_3o_corr2", 3, 2, (2, 3), 3, 24, 300, "uniform"),
 ])
 def test_backward2_against_c_oracle(name, lmax, corr, outs, E, K, N, dist):
     from oracle.contraction import Problem

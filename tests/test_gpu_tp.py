@@ -40,6 +40,8 @@ def _host(*ts):
     ("hidden_0123", 3, (0, 1, 2, 3), 3, 33, [12, 20]),
     ("even_K6", 3, (0, 1), 3, 6, [9, 14]),            # channel pairs with 8-byte async chunks
     ("K96_ragged_pairs", 2, (0, 1), 2, 96, [20, 25]),  # last 64-channel group half full
+    ("K1_scalar", 2, (0,), 2, 1, [5, 6]),
+    ("Y_l0_only", 0, (0, 1, 2), 2, 16, [7, 9]),
 ])
 def test_tp_against_oracle(name, lmax_y, hidden, lmax_out, K, sizes):
     from oracle.tp import TPProblem, forward, backward
