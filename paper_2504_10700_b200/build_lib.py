@@ -20,7 +20,8 @@ SOURCES = ["cg.cpp", "builder.cpp", "codegen.cpp", "pack.cpp", "api.cpp", "tp.cp
 
 # (lmax_in, correlation, out_L): BASELINE configs + the corr-1/2 cases the tests use
 PRESETS = [(3, 3, (0,)), (3, 3, (0, 1)), (3, 3, (0, 1, 2)), (3, 1, (0, 1, 2, 3)), (3, 2, (0,)),
-           (3, 2, (0, 1)), (2, 3, (0, 1)), (1, 3, (0, 1)), (3, 3, (1,))]
+           (3, 2, (0, 1)), (2, 3, (0, 1)), (1, 3, (0, 1)), (3, 3, (1,)), (0, 3, (0,)), (3, 2, (2, 3)),
+           (2, 3, (0, 1, 2, 3))]
 
 
 def _newer(target, deps):
@@ -63,7 +64,8 @@ def build(verbose=False):
 
 # channelwise TP (lmax_y, hidden_l, lmax_out, K): the bench shape and the test configurations
 TP_PRESETS = [(3, (0, 1), 3, 128), (3, (0, 1), 3, 64), (3, (0, 1), 3, 32), (3, (0, 1), 3, 6), (3, (0,), 3, 64),
-              (3, (0, 1, 2), 3, 32), (2, (0, 1), 2, 13), (2, (0, 1), 2, 96), (1, (1,), 1, 40), (3, (0, 1, 2, 3), 3, 33)]
+              (3, (0, 1, 2), 3, 32), (2, (0, 1), 2, 13), (2, (0, 1), 2, 96), (1, (1,), 1, 40), (3, (0, 1, 2, 3), 3, 33),
+              (2, (0,), 2, 1), (0, (0, 1, 2), 2, 16)]
 
 
 def precompile_tp(presets=TP_PRESETS):
