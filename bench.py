@@ -51,6 +51,7 @@ def parse():
                     help="SURVEY §8(f) row 2: channelwise tensor product (Alg. 2) + neighbour sum, forward + "
                          "backward (dY, dh, dR) per step on the bin's molecular graphs (degree 30); "
                          "metric symcon_tp_fwd_bwd_edges_per_s")
+    ap.add_argument("--graph", action="store_true", help="replay the step as a CUDA graph (N=1)")
     ap.add_argument("--double-backward", action="store_true",
                     help="force-training step (SURVEY §8(f) row 1): fwd + bwd + the double backward "
                          "(dB_bar, A_bar, W_bar of <uA, dA>) per step; metric symcon_fwd_bwd_bwd2_nodes_per_s")
@@ -350,6 +351,27 @@ def run_ours(args):
     torch.cuda.synchronize()
     s, bad = sc.check_device_error()
     assert s == 0, (s, bad)
+    if args.graph:
+        # one CUDA graph per pool entry (the whole step: bucketing, fold, fwd, dW || dA, reduce,
+        # unfold); replays remove the per-launch gaps. Launch counts are taken at capture.
+        graphs, per_step = [], []
+        for q in range(POOL):
+            g = torch.cuda.CUDAGraph()
+            n0 = dp.launches
+            with torch.cuda.graph(g):
+                step(q)
+            per_step.append(dp.launches - n0)
+            graphs.append(g)
+        torch.cuda.synchronize()
+        eager_step = step
+
+        def step(q):  # noqa: F811
+            graphs[q % POOL].replay()
+            dp.launches += per_step[q % POOL]
+            return pool[q % POOL][1]
+        for q in range(args.warmup):
+            step(q)
+        torch.cuda.synchronize()
     if getattr(dp, "_peer", None) is not None:
         assert int(dp._peer.err.item()) == 0, "peer all-reduce barrier timed out"
     if world > 1:
