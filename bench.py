@@ -51,7 +51,9 @@ def parse():
                     help="SURVEY §8(f) row 2: channelwise tensor product (Alg. 2) + neighbour sum, forward + "
                          "backward (dY, dh, dR) per step on the bin's molecular graphs (degree 30); "
                          "metric symcon_tp_fwd_bwd_edges_per_s")
-    ap.add_argument("--graph", action="store_true", help="replay the step as a CUDA graph (N=1)")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="launch eagerly (default at N=1: the step is replayed as a CUDA graph; N>1 always eager "
+                         "because the peer all-reduce takes a fresh barrier epoch per call)")
     ap.add_argument("--double-backward", action="store_true",
                     help="force-training step (SURVEY §8(f) row 1): fwd + bwd + the double backward "
                          "(dB_bar, A_bar, W_bar of <uA, dA>) per step; metric symcon_fwd_bwd_bwd2_nodes_per_s")
@@ -351,7 +353,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     s, bad = sc.check_device_error()
     assert s == 0, (s, bad)
-    if args.graph:
+    use_graph = world == 1 and not args.no_graph
+    if use_graph:
         # one CUDA graph per pool entry (the whole step: bucketing, fold, fwd, dW || dA, reduce,
         # unfold); replays remove the per-launch gaps. Launch counts are taken at capture.
         graphs, per_step = [], []
@@ -549,7 +552,7 @@ def run_ours(args):
                                                         "nccl": "NCCL on a communication stream"}[dp.allreduce]
                                                        if world > 1 else None),
                        "seq_len": None, "parallelism": f"dp{world}", "l2": "inputs > L2 (A 410 MB/bin), 4-bin pool",
-                       "alg1_pack_s": round(t_pack, 3)},
+                       "alg1_pack_s": round(t_pack, 3), "cuda_graph": use_graph},
             "per_gpu_nodes_per_s": value / world,
             "per_rank_ms_per_step": per_rank_ms,
             "path_tops": path_ops / (ms_max / args.steps / 1e3) / 1e12,
