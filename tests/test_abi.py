@@ -143,3 +143,13 @@ def test_tp_invalid_arguments(L):
         with pytest.raises(L.SymconError) as e:
             L.symcon_tp_build(args[0], args[1], args[2], 8, -1)
         assert e.value.status == L.SYMCON_EINVAL
+
+
+def test_peer_allreduce_argument_validation(L):
+    # no device work: invalid arguments are rejected before any launch
+    for bufs, rank in (([16] * 9, 0), ([16, 16], 2), ([16, 16], -1), ([], 0)):
+        with pytest.raises(L.SymconError) as e:
+            L.symcon_peer_allreduce(bufs, [16] * len(bufs), rank, 16, 1, 16, None, None)
+        assert e.value.status == L.SYMCON_EINVAL
+    with pytest.raises(L.SymconError):   # NULL peer pointer
+        L.symcon_peer_allreduce([16, None], [16, 16], 0, 16, 1, 16, None, None)
