@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-graph", action="store_true",
                     help="launch eagerly (default at N=1: the step is replayed as a CUDA graph; N>1 always eager "
                          "because the peer all-reduce takes a fresh barrier epoch per call)")
+    ap.add_argument("--graph-all", action="store_true",
+                    help="also replay the step as a CUDA graph at N > 1 (device-side all-reduce epochs)")
     ap.add_argument("--double-backward", action="store_true",
                     help="force-training step (SURVEY §8(f) row 1): fwd + bwd + the double backward "
                          "(dB_bar, A_bar, W_bar of <uA, dA>) per step; metric symcon_fwd_bwd_bwd2_nodes_per_s")
@@ -353,7 +355,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     s, bad = sc.check_device_error()
     assert s == 0, (s, bad)
-    use_graph = world == 1 and not args.no_graph
+    use_graph = (world == 1 or args.graph_all) and not args.no_graph
     if use_graph:
         # one CUDA graph per pool entry (the whole step: bucketing, fold, fwd, dW || dA, reduce,
         # unfold); replays remove the per-launch gaps. Launch counts are taken at capture.

@@ -191,6 +191,11 @@ symcon_status symcon_pack_balanced(const int64_t* sizes, int64_t n, int64_t capa
  * only if no peer reads it afterwards. */
 symcon_status symcon_peer_allreduce(const float* const* bufs, uint32_t* const* pads, int32_t world, int32_t rank,
                                     int64_t n, uint32_t epoch, float* out, int32_t* err, void* stream);
+/* Same, CUDA-graph capturable: the epoch is read on the device from *epoch_counter + 1 (a uint32
+ * in device memory, zero-initialised, one per reducer) and the counter is incremented by a
+ * one-thread kernel launched right after, so a captured call can be replayed. */
+symcon_status symcon_peer_allreduce_dev(const float* const* bufs, uint32_t* const* pads, int32_t world, int32_t rank,
+                                        int64_t n, uint32_t* epoch_counter, float* out, int32_t* err, void* stream);
 
 /* ---- channelwise tensor product + edge->node sum ----------------
  * Alg. 2 of the paper, the message construction that feeds the contraction,

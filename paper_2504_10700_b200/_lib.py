@@ -26,7 +26,7 @@ EXPORTS = ["symcon_build_tables", "symcon_plan_info", "symcon_plan_path", "symco
            "symcon_profile_reset", "symcon_profile_read", "symcon_tp_build", "symcon_tp_info", "symcon_tp_path",
            "symcon_tp_workspace_bytes", "symcon_tp_forward", "symcon_tp_backward", "symcon_tp_check_device_error",
            "symcon_tp_last_launch_count", "symcon_tp_source", "symcon_tp_destroy", "symcon_peer_allreduce",
-           "symcon_tp_precompile"]
+           "symcon_tp_precompile", "symcon_peer_allreduce_dev"]
 
 
 class SymconInfo(ctypes.Structure):
@@ -302,3 +302,15 @@ def symcon_peer_allreduce(bufs, pads, rank, n, epoch, out, err, stream):
     b = (_vp * world)(*bufs)
     p = (_vp * world)(*pads)
     check(lib.symcon_peer_allreduce(b, p, world, rank, n, epoch, out, err, stream), "symcon_peer_allreduce")
+
+
+lib.symcon_peer_allreduce_dev.argtypes = [_vp, _vp, _i32, _i32, _i64, _vp, _vp, _vp, _vp]
+lib.symcon_peer_allreduce_dev.restype = ctypes.c_int
+
+
+def symcon_peer_allreduce_dev(bufs, pads, rank, n, epoch_counter, out, err, stream):
+    world = len(bufs)
+    b = (_vp * world)(*bufs)
+    p = (_vp * world)(*pads)
+    check(lib.symcon_peer_allreduce_dev(b, p, world, rank, n, epoch_counter, out, err, stream),
+          "symcon_peer_allreduce_dev")

@@ -737,8 +737,22 @@ symcon_status symcon_backward2(const symcon_plan* p, int64_t N, const float* A, 
   return cuda_err(cudaGetLastError(), "backward2 launch");
 }
 
+static symcon_status peer_common(const float* const* bufs, uint32_t* const* pads, int32_t world, int32_t rank,
+                                 int64_t n, uint32_t epoch, uint32_t* epoch_dev, float* out, int32_t* err, void* stream);
+
 symcon_status symcon_peer_allreduce(const float* const* bufs, uint32_t* const* pads, int32_t world, int32_t rank,
                                     int64_t n, uint32_t epoch, float* out, int32_t* err, void* stream) {
+  return peer_common(bufs, pads, world, rank, n, epoch, nullptr, out, err, stream);
+}
+
+symcon_status symcon_peer_allreduce_dev(const float* const* bufs, uint32_t* const* pads, int32_t world, int32_t rank,
+                                        int64_t n, uint32_t* epoch_counter, float* out, int32_t* err, void* stream) {
+  if (!epoch_counter) { set_error("NULL epoch counter"); return SYMCON_EINVAL; }
+  return peer_common(bufs, pads, world, rank, n, 0, epoch_counter, out, err, stream);
+}
+
+static symcon_status peer_common(const float* const* bufs, uint32_t* const* pads, int32_t world, int32_t rank,
+                                 int64_t n, uint32_t epoch, uint32_t* epoch_dev, float* out, int32_t* err, void* stream) {
   if (!bufs || !pads || !out || world < 1 || world > 8 || rank < 0 || rank >= world || n < 0) {
     set_error("bad peer all-reduce arguments");
     return SYMCON_EINVAL;
@@ -759,7 +773,7 @@ symcon_status symcon_peer_allreduce(const float* const* bufs, uint32_t* const* p
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long n4 = (n + 3) / 4;
   const int blocks = (int)std::max<long long>(1, std::min<long long>(sms, (n4 + 511) / 512));
-  peer_allreduce_launch(a, world, rank, n, epoch, out, err, blocks, (cudaStream_t)stream);
+  peer_allreduce_launch(a, world, rank, n, epoch, epoch_dev, out, err, blocks, (cudaStream_t)stream);
   return cuda_err(cudaGetLastError(), "peer all-reduce launch");
 }
 

@@ -35,8 +35,8 @@ struct PeerArgs {
   const float* buf[8];   // each rank's symmetric dW buffer (peer pointers)
   unsigned* pad[8];      // each rank's signal pad (uint32 flags, slot r written by rank r)
 };
-int peer_allreduce_launch(const PeerArgs& a, int world, int rank, long long n, unsigned epoch, float* out, int* err,
-                          int blocks, cudaStream_t st);
+int peer_allreduce_launch(const PeerArgs& a, int world, int rank, long long n, unsigned epoch, unsigned* epoch_dev,
+                          float* out, int* err, int blocks, cudaStream_t st);
 
 // channelwise TP (tp_static.cu)
 struct TPCsrArgs {

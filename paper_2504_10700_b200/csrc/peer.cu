@@ -19,8 +19,13 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
   return v;
 }
 
-__global__ void __launch_bounds__(512) peer_allreduce(PeerArgs a, int world, int rank, long long n, unsigned epoch,
-                                                      float* __restrict__ out, int* err) {
+__global__ void peer_epoch_bump(unsigned* counter) { *counter += 1u; }
+
+__global__ void __launch_bounds__(512) peer_allreduce(PeerArgs a, int world, int rank, long long n, unsigned epoch_host,
+                                                      const unsigned* epoch_dev, float* __restrict__ out, int* err) {
+  // epoch from the host argument, or (graph-capturable form) the device counter + 1; the counter
+  // is bumped by a separate one-thread kernel after this one, so every block reads the same value
+  const unsigned epoch = epoch_dev ? *epoch_dev + 1u : epoch_host;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     __threadfence_system();   // this rank's partial (written by earlier kernels) visible to the peers
     for (int p = 0; p < world; p++) st_release_sys(a.pad[p] + rank, epoch);
@@ -53,9 +58,13 @@ __global__ void __launch_bounds__(512) peer_allreduce(PeerArgs a, int world, int
 
 }  // namespace
 
-int peer_allreduce_launch(const PeerArgs& a, int world, int rank, long long n, unsigned epoch, float* out, int* err,
-                          int blocks, cudaStream_t st) {
-  peer_allreduce<<<blocks, 512, 0, st>>>(a, world, rank, n, epoch, out, err);
+int peer_allreduce_launch(const PeerArgs& a, int world, int rank, long long n, unsigned epoch, unsigned* epoch_dev,
+                          float* out, int* err, int blocks, cudaStream_t st) {
+  peer_allreduce<<<blocks, 512, 0, st>>>(a, world, rank, n, epoch, epoch_dev, out, err);
+  if (epoch_dev) {
+    peer_epoch_bump<<<1, 1, 0, st>>>(epoch_dev);
+    return 2;
+  }
   return 1;
 }
 

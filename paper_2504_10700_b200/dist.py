@@ -66,6 +66,7 @@ class PeerReducer:
         pad = self.hdl[0].get_signal_pad(self.rank, (self.world,), dtype=torch.int32)
         pad.zero_()
         self.err = torch.zeros(1, dtype=torch.int32, device=device)
+        self.counter = torch.zeros(1, dtype=torch.int32, device=device)   # device epoch (graph-capturable)
         torch.cuda.synchronize(device)
         dist.barrier(group=group)
         self.epoch = 0
@@ -75,10 +76,11 @@ class PeerReducer:
         return self.bufs[self.parity]
 
     def allreduce(self, out, stream):
-        self.epoch += 1
+        """Epoch kept on the device (symcon_peer_allreduce_dev), so the call can be captured in a
+        CUDA graph; the buffer parity alternates per call (capture an even number of steps)."""
         h = self.hdl[self.parity]
-        _lib.symcon_peer_allreduce(list(h.buffer_ptrs), list(self.hdl[0].signal_pad_ptrs), self.rank, self.numel,
-                                   self.epoch, out.data_ptr(), self.err.data_ptr(), stream)
+        _lib.symcon_peer_allreduce_dev(list(h.buffer_ptrs), list(self.hdl[0].signal_pad_ptrs), self.rank, self.numel,
+                                       self.counter.data_ptr(), out.data_ptr(), self.err.data_ptr(), stream)
         self.parity ^= 1
         return out
 
