@@ -373,8 +373,11 @@ def run_ours(args):
         def step(q):  # noqa: F811
             graphs[q % POOL].replay()
             dp.launches += per_step[q % POOL]
+            if getattr(dp, "_peer", None) is not None:
+                # graph q was captured with buffer parity q % 2; keep eager calls alternating too
+                dp._peer.parity = (q + 1) % 2
             return pool[q % POOL][1]
-        for q in range(args.warmup):
+        for q in range(POOL):   # a whole cycle, so the timed replays continue the buffer alternation
             step(q)
         torch.cuda.synchronize()
     if getattr(dp, "_peer", None) is not None:

@@ -55,8 +55,11 @@ class PeerReducer:
     def __init__(self, numel, device, group=None):
         import torch.distributed._symmetric_memory as symm
         grp = group if group is not None else dist.group.WORLD
+        import warnings
         try:
-            symm.enable_symm_mem_for_group(grp.group_name)
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                symm.enable_symm_mem_for_group(grp.group_name)
         except Exception:  # noqa: BLE001  (newer torch: not needed)
             pass
         self.numel = int(numel)
