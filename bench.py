@@ -1,18 +1,22 @@
 """Benchmark: symmetric-contraction fwd+bwd nodes/s on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config mp_medium]
+                    [--capacity C]
 
 A step is one pass of the whole hot path over one bin of molecular graphs per GPU:
 element bucketing, W-fold, forward B, backward dW (S partials + fixed-order reduction) and
-dA, and — for N > 1 — the NCCL all-reduce of dW. Workload (SURVEY.md §8(d) config 5 at the
-MP-medium shape): the 2,650,823-graph Table-2 manifest packed by Alg. 1 (C++ partitioner,
-capacity 50,000 nodes, M = multiple of N bins), bin s*N + r on rank r at step s; 128
-channels, 0e+1o output, lmax 3, correlation 3, 89 elements (1-4 Zipf elements per graph).
-Inputs for the timed steps are resident in HBM before timing; A alone is 410 MB per bin,
-larger than L2, and a pool of distinct bins is cycled, so no L2 flush is needed.
+dA, and -- for N > 1 -- the dW all-reduce (libsymcon's NVLink peer-memory kernel). Workload
+(SURVEY.md §8(d) config 5 at the MP-medium shape): the 2,650,823-graph Table-2 manifest packed
+by Alg. 1 (C++ partitioner, capacity C = 50,000 nodes by default, 3,072 = the paper's operating
+point PAPER.md:969 with --capacity 3072, M = multiple of N bins), bin s*N + r on rank r at step s;
+128 channels, 0e+1o output, lmax 3, correlation 3, 89 elements (1-4 Zipf elements per graph).
+Inputs for the timed steps are resident in HBM before timing; A alone is 410 MB per 50k-node bin,
+larger than L2, and a pool of distinct bins is cycled (at C = 3072 the 4-bin pool is L2-resident;
+the line says so).
 
-One JSON line on rank 0. `roofline` reports the dominant kernel (FP32 ALU bound), its
-per-launch CUDA-event time measured by libsymcon's launch timer inside the timed region.
+The exact timed step is `TimedStep` (also driven by tests/test_gpu_timed_step.py, which checks
+its outputs against the oracle). One JSON line on rank 0. `roofline` reports the dominant
+kernel, its per-launch CUDA-event time measured by libsymcon's launch timer.
 """
 import argparse
 import json
@@ -31,35 +35,39 @@ sys.path.insert(0, ROOT)
 
 CAPACITY = 50_000
 POOL = 4
+EDGE_DEGREE = 30   # synthetic in-degree min(30, n-1)
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="mp_medium", choices=["off_small", "mp_medium", "large"])
+    ap.add_argument("--capacity", type=int, default=CAPACITY,
+                    help="Alg. 1 bin capacity in nodes per GPU-step (paper: 3072, PAPER.md:969)")
     ap.add_argument("--cpu-sample", type=int, default=32768, help="nodes in the oracle's bounded sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-overlap", action="store_true", help="all-reduce dW after dA instead of overlapping")
     ap.add_argument("--allreduce", default="peer", choices=["peer", "nccl"],
                     help="N > 1: dW all-reduce by libsymcon's NVLink peer-memory kernel (default) or NCCL")
+    ap.add_argument("--peer-algo", type=int, default=0, choices=[0, 1, 2],
+                    help="peer all-reduce: 0 auto (two-shot at N >= 4), 1 one-shot, 2 two-shot")
     ap.add_argument("--sequential-bwd", action="store_true", help="run the dW and dA kernels back to back on one stream")
-    ap.add_argument("--concurrent-bwd", action="store_true", help="run dA on a side stream concurrent with dW (default at N=1)")
+    ap.add_argument("--concurrent-bwd", action="store_true", help="run dA on a side stream concurrent with dW (default)")
     ap.add_argument("--channelwise-tp", action="store_true",
                     help="SURVEY §8(f) row 2: channelwise tensor product (Alg. 2) + neighbour sum, forward + "
                          "backward (dY, dh, dR) per step on the bin's molecular graphs (degree 30); "
                          "metric symcon_tp_fwd_bwd_edges_per_s")
     ap.add_argument("--no-graph", action="store_true",
-                    help="launch eagerly (default at N=1: the step is replayed as a CUDA graph; N>1 always eager "
-                         "because the peer all-reduce takes a fresh barrier epoch per call)")
+                    help="launch eagerly (default at N=1: the step is replayed as a CUDA graph)")
     ap.add_argument("--graph-all", action="store_true",
                     help="also replay the step as a CUDA graph at N > 1 (device-side all-reduce epochs)")
     ap.add_argument("--double-backward", action="store_true",
                     help="force-training step (SURVEY §8(f) row 1): fwd + bwd + the double backward "
                          "(dB_bar, A_bar, W_bar of <uA, dA>) per step; metric symcon_fwd_bwd_bwd2_nodes_per_s")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 # ----------------------------------------------------------------------------- workload
@@ -68,20 +76,62 @@ def shape_of(name):
     return CONFIGS[name]
 
 
-def plan_bins(world, seed=0):
-    """Alg. 1 over the Table-2 manifest (same plan on every rank: deterministic)."""
+def plan_bins(world, capacity=CAPACITY, seed=0):
+    """Alg. 1 over the Table-2 manifest with libsymcon's C++ partitioner (GPU arm; same plan on
+    every rank: deterministic)."""
     from synth.inputs import table2_sizes
     from paper_2504_10700_b200 import _lib
     sizes = table2_sizes(seed=seed)
     t0 = time.time()
-    offs, ids = _lib.symcon_pack_balanced(sizes, CAPACITY, world)
+    offs, ids = _lib.symcon_pack_balanced(sizes, capacity, world)
     return sizes, offs, ids, time.time() - t0
+
+
+def plan_bins_oracle(world, capacity=CAPACITY, seed=0):
+    """The same plan from the oracle's Alg. 1 (oracle/packing.py; reference arm -- no product code).
+    tests/test_abi.py pins the two partitioners to identical bins."""
+    from synth.inputs import table2_sizes
+    from oracle.packing import create_balanced_batches
+    sizes = table2_sizes(seed=seed)
+    bins = create_balanced_batches([int(x) for x in sizes], capacity, world)
+    offs = np.zeros(len(bins) + 1, np.int64)
+    offs[1:] = np.cumsum([len(b) for b in bins])
+    ids = np.array([g for b in bins for g in b], np.int64)
+    return sizes, offs, ids
 
 
 def bin_elements(sizes, offs, ids, b, n_elements):
     from synth.inputs import graph_elements
     g = ids[offs[b]:offs[b + 1]]
     return graph_elements(sizes[g], n_elements=n_elements, seed=0, salt=int(b))
+
+
+def bin_inputs(cfg, sizes, offs, ids, b, q, rank, out_dim, n_lm, device):
+    """(node_elem, A, dB) of bin b as pool entry q of `rank`: the same seeded values for the GPU arm
+    and the oracle (synth draws on the CPU, then moves to `device`)."""
+    import torch
+    from synth.inputs import gen_A, gen_dB
+    ne = torch.from_numpy(bin_elements(sizes, offs, ids, b, cfg.n_elements)).to(device)
+    N = ne.numel()
+    A = gen_A(N, cfg.channels, n_lm, device, seed=100 * q + rank)
+    dB = gen_dB(N, out_dim, device, seed=100 * q + rank)
+    return ne, A, dB
+
+
+def edge_spread(sizes, offs, ids, world, steps):
+    """Secondary balance metric (north_star: "balancing node and edge counts per GPU"): per step,
+    max/mean over ranks of the bins' synthetic edge counts (degree min(30, n-1))."""
+    from synth.inputs import graph_edges
+    n_bins = len(offs) - 1
+    worst, mean = 1.0, []
+    for st in range(min(steps, n_bins // world)):
+        e = [int(graph_edges(sizes[ids[offs[st * world + r]:offs[st * world + r + 1]]], EDGE_DEGREE).sum())
+             for r in range(world)]
+        m = max(float(np.mean(e)), 1.0)
+        worst = max(worst, max(e) / m)
+        mean.append(m)
+    return {"edges_per_bin_mean": float(np.mean(mean)) if mean else 0.0, "edge_imbalance_max_over_mean": worst,
+            "degree": f"min({EDGE_DEGREE}, n-1) per node"}
 
 
 def alg_ops(sc):
@@ -120,7 +170,7 @@ def alg_ops(sc):
             "prefixes": len(prefixes), "deg3_monomials": deg3, "n_sym": int(len(L))}
 
 
-def path_roofline(cfg, sc, mean_nodes, path_ops, ms_step, dbl):
+def path_roofline(cfg, sc, mean_nodes, path_ops, ms_step, dbl, sm_mhz=1965.0):
     """Whole-step roofline: the step's algorithmic FP32 lane-ops at the ALU peak vs its
     algorithmic HBM bytes at the measured copy bandwidth (A read twice, dB, B and dA
     once per node-channel; the double backward adds uA, A, dB reads and dB_bar, A_bar writes)."""
@@ -132,11 +182,11 @@ def path_roofline(cfg, sc, mean_nodes, path_ops, ms_step, dbl):
         per += 4 * (3 * nlm + outc + outc + nlm)
     hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6553.0
-    t_alu = path_ops / (148 * 128 * 1.965e9)
+    t_alu = path_ops / (148 * 128 * sm_mhz * 1e6)
     t_hbm = per * mean_nodes * K / (hbm * 1e9)
     bound = "alu" if t_alu >= t_hbm else "hbm"
     return {"bound": bound, "frac": max(t_alu, t_hbm) / (ms_step / 1e3), "t_alu_ms": t_alu * 1e3, "t_hbm_ms": t_hbm * 1e3,
-            "bytes_per_node_channel": per}
+            "bytes_per_node_channel": per, "sm_mhz": sm_mhz}
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -225,8 +275,9 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- cpu oracle
-def cpu_baseline(cfg, sc, A, W, ne, dB, n_sample, seed=0):
-    """The oracle's plain C fp64 loop (never tuned) on a bounded sample of the workload."""
+def cpu_baseline(cfg, A, W, ne, dB, n_sample, seed=0, single_sample=512):
+    """The oracle's plain C fp64 loop (never tuned) on a bounded sample of the workload: all cores
+    of the affinity mask, and one thread on a smaller sample."""
     from oracle.contraction import Problem
     from oracle.ceval import OracleC
     oc = OracleC(Problem(cfg.lmax_in, cfg.correlation, cfg.out_L))
@@ -240,50 +291,168 @@ def cpu_baseline(cfg, sc, A, W, ne, dB, n_sample, seed=0):
     oc.forward(hA, hW, hne)
     oc.backward(hA, hW, hne, hdB)
     dt = time.time() - t0
-    return {"value": len(idx) / dt, "unit": "nodes/s", "cores": oc.threads(), "kind": "oracle",
+    cores = oc.threads()
+    n1 = min(single_sample, len(idx))
+    oc.lib.oracle_set_threads(1)
+    t1 = time.time()
+    oc.forward(hA[:n1], hW, hne[:n1])
+    oc.backward(hA[:n1], hW, hne[:n1], hdB[:n1])
+    dt1 = time.time() - t1
+    oc.lib.oracle_set_threads(cores)
+    import platform
+    model = next((ln.split(":", 1)[1].strip() for ln in open("/proc/cpuinfo") if ln.startswith("model name")), platform.processor())
+    return {"value": len(idx) / dt, "unit": "nodes/s", "cores": cores, "kind": "oracle",
             "sample": f"{len(idx)} random nodes of one {A.shape[0]}-node bin, fwd+bwd (B, dA, dW), fp64 C/OpenMP loop "
-                      f"over {oc.n_terms} raw U terms per (node, channel), {dt:.1f} s"}
+                      f"over {oc.n_terms} raw U terms per (node, channel), {dt:.1f} s",
+            "single_thread": {"value": n1 / dt1, "unit": "nodes/s", "cores": 1, "sample": f"first {n1} nodes of the sample, {dt1:.1f} s"},
+            "cpu_model": model}
 
 
 def run_reference(args):
-    """--impl reference: the oracle on the host cores, each step a bounded sample of the workload."""
+    """--impl reference: the oracle (oracle/ only: Alg. 1 from oracle/packing.py, the plain C fp64
+    evaluator) on the host cores. Same workload as the GPU arm's first pool entry on rank 0: the same
+    Alg. 1 bin, the same seeded node elements, A and dB; each step a bounded sample of its nodes."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import torch
-    from synth.inputs import gen_A, gen_W, gen_dB
+    from synth.inputs import gen_W
     from oracle.contraction import Problem
     from oracle.ceval import OracleC
     cfg = shape_of(args.config)
     prob = Problem(cfg.lmax_in, cfg.correlation, cfg.out_L)
     oc = OracleC(prob)
-    sizes, offs, ids, _ = plan_bins(max(args.gpus, 1))
-    ne_full = bin_elements(sizes, offs, ids, 0, cfg.n_elements)
-    n_bin = len(ne_full)
-    per_step = max(64, args.cpu_sample // 8)
-    A = gen_A(per_step, cfg.channels, 16, "cpu").numpy()
-    W = gen_W(cfg.n_elements, prob.block_sizes(), cfg.channels, "cpu").numpy()
-    dB = gen_dB(per_step, prob.out_dim(cfg.channels), "cpu").numpy()
-    ne = ne_full[:per_step]
-    for _ in range(args.warmup):
-        oc.forward(A[:16], W, ne[:16])
+    world = max(args.gpus, 1)
     t0 = time.time()
-    for _ in range(args.steps):
-        oc.forward(A, W, ne)
-        oc.backward(A, W, ne, dB)
+    sizes, offs, ids = plan_bins_oracle(world, args.capacity)
+    t_pack = time.time() - t0
+    b = 0   # pool entry 0 of rank 0 = step 0's bin of rank 0
+    n_lm = (cfg.lmax_in + 1) ** 2
+    ne_t, A_t, dB_t = bin_inputs(cfg, sizes, offs, ids, b, 0, 0, prob.out_dim(cfg.channels), n_lm, "cpu")
+    ne_full, A_full, dB_full = ne_t.numpy(), A_t.numpy(), dB_t.numpy()
+    n_bin = len(ne_full)
+    W = gen_W(cfg.n_elements, prob.block_sizes(), cfg.channels, "cpu").numpy()
+    per_step = max(64, min(n_bin, args.cpu_sample // 8))
+    perm = np.random.default_rng(0).permutation(n_bin)
+
+    def sample(q):
+        idx = np.sort(perm[(q * per_step) % n_bin:][:per_step])
+        return A_full[idx], ne_full[idx], dB_full[idx]
+    for q in range(args.warmup):
+        a, e, d = sample(q)
+        oc.forward(a[:16], W, e[:16])
+    t0 = time.time()
+    for q in range(args.steps):
+        a, e, d = sample(q)
+        oc.forward(a, W, e)
+        oc.backward(a, W, e, d)
     dt = time.time() - t0
     v = per_step * args.steps / dt
     out = {"impl": "reference", "metric": "symcon_fwd_bwd_nodes_per_s", "value": v, "unit": "nodes/s",
            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"{args.config}_dp_step", "nodes_per_bin": n_bin, "channels": cfg.channels,
-                      "out": "+".join(f"{L}{'e' if L % 2 == 0 else 'o'}" for L in cfg.out_L), "lmax_in": cfg.lmax_in,
-                      "correlation": cfg.correlation, "elements": cfg.n_elements,
-                      "sample": f"{per_step} nodes of bin 0 per step"},
+           "config": workload_config(args, cfg, n_bin),
+           "same_config": True,
            "cpu_baseline": {"value": v, "unit": "nodes/s", "cores": oc.threads(), "kind": "oracle",
-                            "sample": f"{per_step} nodes per step x {args.steps} steps"},
+                            "sample": f"{per_step} nodes per step (seeded permutation of bin 0, the GPU arm's pool entry 0 "
+                                      f"on rank 0: same Alg. 1 bin, node elements, A, dB, W) x {args.steps} steps"},
+           "alg1_pack_s": round(t_pack, 3), "oracle_only": "oracle/packing.py + oracle/csrc/oracle_eval.c; libsymcon not loaded",
            "e2e": {"value": v, "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
+
+
+def workload_config(args, cfg, nodes_per_bin):
+    return {"workload": f"{args.config}_dp_step" + ("_double_backward" if args.double_backward else "")
+                        + ("" if args.capacity == CAPACITY else f"_C{args.capacity}"),
+            "model": "MACE symmetric contraction", "channels": cfg.channels,
+            "out": "+".join(f"{cfg.channels}x{L}{'e' if L % 2 == 0 else 'o'}" for L in cfg.out_L),
+            "lmax_in": cfg.lmax_in, "correlation": cfg.correlation, "elements": cfg.n_elements,
+            "capacity_nodes": args.capacity, "nodes_bin0": int(nodes_per_bin)}
+
+
+# ----------------------------------------------------------------------------- the timed step
+class TimedStep:
+    """The step bench.py times, on this rank: a pool of `pool` distinct Alg. 1 bins resident in
+    HBM (bin of step q % n_steps for this rank), W replicated, one DataParallelContraction
+    (dW on the main stream, dA concurrently on a side stream sharing the workspace, reuse hints
+    after the forward, and for N > 1 the dW all-reduce), optionally replayed from one CUDA graph
+    per pool entry. tests/test_gpu_timed_step.py drives this very object and checks its outputs
+    against the oracle."""
+
+    def __init__(self, config="mp_medium", capacity=CAPACITY, world=1, rank=0, device=0, pool=POOL,
+                 double_backward=False, allreduce="peer", peer_algo=0, overlap=True, concurrent_bwd=None):
+        import torch
+        from paper_2504_10700_b200.ops import SymmetricContraction
+        from paper_2504_10700_b200.dist import BinPackedShards, DataParallelContraction
+        from synth.inputs import gen_A, gen_W, table2_sizes
+        self.torch = torch
+        self.cfg = cfg = shape_of(config)
+        self.dev = dev = torch.device("cuda", device)
+        self.world, self.rank, self.double_backward = world, rank, double_backward
+        self.sc = sc = SymmetricContraction(cfg.lmax_in, cfg.correlation, cfg.out_L, cfg.n_elements, cfg.channels,
+                                            device=device)
+        self.sizes = table2_sizes(seed=0)
+        t0 = time.time()
+        self.shards = BinPackedShards(self.sizes, capacity, world, rank)
+        self.t_pack = time.time() - t0
+        self.pool, self.uA = [], {}
+        for q in range(pool):
+            b = self.shards.bin_of(q % self.shards.n_steps)
+            ne, A, dB = bin_inputs(cfg, self.sizes, self.shards.offsets, self.shards.ids, b, q, rank, sc.out_dim,
+                                   sc.n_lm, dev)
+            N = ne.numel()
+            B = torch.empty((N, sc.out_dim), device=dev)
+            dA = torch.empty_like(A)
+            self.pool.append((b, N, A, ne, dB, B, dA))
+            if double_backward:
+                self.uA[q] = gen_A(N, cfg.channels, sc.n_lm, dev, seed=100 * q + rank + 7)
+        self.imbalance = max(self.shards.step_imbalance(q % self.shards.n_steps) for q in range(pool))
+        self.W = gen_W(cfg.n_elements, sc.block_sizes(), cfg.channels, dev)
+        if world > 1:
+            import torch.distributed as dist
+            dist.broadcast(self.W, 0)
+        self.dW = torch.empty_like(self.W)
+        for q in range(pool):
+            sc.workspace(self.pool[q][1])
+        self.dp = DataParallelContraction(sc, overlap=overlap, concurrent_bwd=concurrent_bwd, allreduce=allreduce,
+                                          peer_algo=peer_algo)
+        self.graphs = None
+        self.outputs = {}   # q -> (B, dA, dW[, W_bar]) of the last call for pool entry q (views; dW shared)
+
+    def eager(self, q, runner=None):
+        dp = runner or self.dp
+        b, N, A, ne, dB, B, dA = self.pool[q % len(self.pool)]
+        dp.forward(A, self.W, ne, B=B)
+        dp.backward(A, self.W, ne, dB, dA=dA, dW=self.dW)
+        if self.double_backward:
+            dp.backward2(A, self.W, ne, dB, self.uA[q % len(self.pool)])
+        return N
+
+    def capture(self):
+        """One CUDA graph per pool entry (the whole step); launch counts taken at capture."""
+        torch = self.torch
+        self.graphs, self.per_step = [], []
+        for q in range(len(self.pool)):
+            g = torch.cuda.CUDAGraph()
+            n0 = self.dp.launches
+            with torch.cuda.graph(g):
+                self.eager(q)
+            self.per_step.append(self.dp.launches - n0)
+            self.graphs.append(g)
+        torch.cuda.synchronize()
+        for q in range(len(self.pool)):   # a whole cycle, so the timed replays continue the buffer alternation
+            self.step(q)
+        torch.cuda.synchronize()
+
+    def step(self, q):
+        if self.graphs is None:
+            return self.eager(q)
+        self.graphs[q % len(self.pool)].replay()
+        self.dp.launches += self.per_step[q % len(self.pool)]
+        for r in (self.dp._peer, self.dp._peer2):
+            if r is not None:
+                # graph q was captured with buffer parity q % 2; keep eager calls alternating too
+                r.parity = (q + 1) % 2
+        return self.pool[q % len(self.pool)][1]
 
 
 # ----------------------------------------------------------------------------- ours
@@ -299,89 +468,22 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    from paper_2504_10700_b200.ops import SymmetricContraction
     from paper_2504_10700_b200 import _lib
-    from synth.inputs import gen_A, gen_W, gen_dB
+    from paper_2504_10700_b200.dist import DataParallelContraction
     cfg = shape_of(args.config)
-    sc = SymmetricContraction(cfg.lmax_in, cfg.correlation, cfg.out_L, cfg.n_elements, cfg.channels, device=local)
-
-    from paper_2504_10700_b200.dist import BinPackedShards, DataParallelContraction
-    from synth.inputs import table2_sizes
-    sizes = table2_sizes(seed=0)
-    t0 = time.time()
-    shards = BinPackedShards(sizes, CAPACITY, world, rank)
-    t_pack = time.time() - t0
-    n_bins = shards.n_bins
-    # pool of distinct bins for this rank (cycled): steps 0..POOL-1 of the epoch
-    pool = []
-    uA = {}
-    for q in range(POOL):
-        step_id = q % shards.n_steps
-        b = shards.bin_of(step_id)
-        ne = torch.from_numpy(bin_elements(sizes, shards.offsets, shards.ids, b, cfg.n_elements)).to(dev)
-        N = ne.numel()
-        A = gen_A(N, cfg.channels, sc.n_lm, dev, seed=100 * q + rank)
-        dB = gen_dB(N, sc.out_dim, dev, seed=100 * q + rank)
-        B = torch.empty((N, sc.out_dim), device=dev)
-        dA = torch.empty_like(A)
-        pool.append((b, N, A, ne, dB, B, dA))
-        if args.double_backward:
-            uA[q] = gen_A(N, cfg.channels, sc.n_lm, dev, seed=100 * q + rank + 7)
-    imbalance = max(shards.step_imbalance(q % shards.n_steps) for q in range(POOL))
-    W = gen_W(cfg.n_elements, sc.block_sizes(), cfg.channels, dev)
-    if world > 1:
-        dist.broadcast(W, 0)
-    dW = torch.empty_like(W)
-    for q in range(POOL):
-        sc.workspace(pool[q][1])
     conc = False if args.sequential_bwd else (True if args.concurrent_bwd else None)
-    dp = DataParallelContraction(sc, overlap=not args.no_overlap, concurrent_bwd=conc, allreduce=args.allreduce)
-
-    def bwd2(q, A, ne, dB, runner):
-        # double backward of the same step (force loss): uA terms through symcon_backward2, W_bar
-        # all-reduced over ranks like dW
-        runner.backward2(A, W, ne, dB, uA[q % POOL])
-
-    def step(q):
-        b, N, A, ne, dB, B, dA = pool[q % POOL]
-        dp.forward(A, W, ne, B=B)
-        dp.backward(A, W, ne, dB, dA=dA, dW=dW)
-        if args.double_backward:
-            bwd2(q, A, ne, dB, dp)
-        return N
-
+    ts = TimedStep(args.config, args.capacity, world, rank, local, POOL, args.double_backward, args.allreduce,
+                   args.peer_algo, not args.no_overlap, conc)
+    sc, dp, W, dW, pool = ts.sc, ts.dp, ts.W, ts.dW, ts.pool
     for q in range(args.warmup):
-        step(q)
+        ts.eager(q)
     torch.cuda.synchronize()
     s, bad = sc.check_device_error()
     assert s == 0, (s, bad)
     use_graph = (world == 1 or args.graph_all) and not args.no_graph
     if use_graph:
-        # one CUDA graph per pool entry (the whole step: bucketing, fold, fwd, dW || dA, reduce,
-        # unfold); replays remove the per-launch gaps. Launch counts are taken at capture.
-        graphs, per_step = [], []
-        for q in range(POOL):
-            g = torch.cuda.CUDAGraph()
-            n0 = dp.launches
-            with torch.cuda.graph(g):
-                step(q)
-            per_step.append(dp.launches - n0)
-            graphs.append(g)
-        torch.cuda.synchronize()
-        eager_step = step
-
-        def step(q):  # noqa: F811
-            graphs[q % POOL].replay()
-            dp.launches += per_step[q % POOL]
-            if getattr(dp, "_peer", None) is not None:
-                # graph q was captured with buffer parity q % 2; keep eager calls alternating too
-                dp._peer.parity = (q + 1) % 2
-            return pool[q % POOL][1]
-        for q in range(POOL):   # a whole cycle, so the timed replays continue the buffer alternation
-            step(q)
-        torch.cuda.synchronize()
-    if getattr(dp, "_peer", None) is not None:
-        assert int(dp._peer.err.item()) == 0, "peer all-reduce barrier timed out"
+        ts.capture()
+    dp.check()   # raises if a peer all-reduce barrier timed out (dW / W_bar then NaN)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -398,30 +500,38 @@ def run_ours(args):
         clk.start()
         e0.record()
         for q in range(args.steps):
-            nodes += step(q)
+            nodes += ts.step(q)
         e1.record()
         torch.cuda.synchronize()
         clk.end()
     if world > 1:
         dist.barrier()
-    if getattr(dp, "_peer", None) is not None:
-        assert int(dp._peer.err.item()) == 0, "peer all-reduce barrier timed out"
+    dp.check()
     ms = e0.elapsed_time(e1)
+    launches_timed = dp.launches
     # per-kernel times for the roofline: a separate pass with the kernels back to back on one
     # stream (the throughput region above overlaps dW and dA, which would blur each kernel's time)
     _lib.symcon_profile_enable(sc.plan, 1)
     _lib.symcon_profile_reset(sc.plan)
     seq = DataParallelContraction(sc, overlap=not args.no_overlap, concurrent_bwd=False, allreduce="nccl")
-    launches_timed = dp.launches
     for q in range(args.steps):
-        b_, N_, A_, ne_, dB_, B_, dA_ = pool[q % POOL]
-        seq.forward(A_, W, ne_, B=B_)
-        seq.backward(A_, W, ne_, dB_, dA=dA_, dW=dW)
-        if args.double_backward:
-            bwd2(q, A_, ne_, dB_, seq)
+        ts.eager(q, runner=seq)
     torch.cuda.synchronize()
     prof = _lib.symcon_profile_read(sc.plan)
     _lib.symcon_profile_enable(sc.plan, 0)
+    # the all-reduce alone (N > 1): device time per call on the main stream
+    ar_ms = None
+    if world > 1 and dp._peer is not None:
+        dist.barrier()
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(10):
+            dp._peer.allreduce(dW, torch.cuda.current_stream().cuda_stream)
+        a1.record()
+        torch.cuda.synchronize()
+        dp.check()
+        ar_ms = a0.elapsed_time(a1) / 10
     t = torch.tensor([ms, nodes], dtype=torch.float64, device=dev)
     if world > 1:
         tt = [torch.zeros_like(t) for _ in range(world)]
@@ -438,7 +548,7 @@ def run_ours(args):
     b, N, A, ne, dB, B, dA = pool[0]
     hA, hne, hdB = A.cpu().pin_memory(), ne.cpu().pin_memory(), dB.cpu().pin_memory()
     hdW = torch.empty(W.shape, dtype=W.dtype).pin_memory()
-    hU = uA[0].cpu().pin_memory() if args.double_backward else None
+    hU = ts.uA[0].cpu().pin_memory() if args.double_backward else None
     dA2 = torch.empty_like(A)
     # two device input sets: the host->device copy of step s+1 (copy stream) overlaps the compute
     # of step s; every step still copies its own inputs and reads its dW back inside the region
@@ -485,6 +595,7 @@ def run_ours(args):
     e2e_run(e2e_steps)
     f1.record()
     torch.cuda.synchronize()
+    dp.check()
     e2e_ms = f0.elapsed_time(f1) / e2e_steps
     t2 = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -497,73 +608,43 @@ def run_ours(args):
         ops = alg_ops(sc)
         K = cfg.channels
         clocks = clk.summary()
-        # dominant kernel by measured time
-        kern = max(prof, key=lambda k: prof[k][1]) if prof else None
-        roof = None
-        if kern:
-            cnt, tot_ms = prof[kern]
-            avg_ms = tot_ms / max(cnt, 1)
-            per_nc = {"symcon_fwd": ops["fwd"], "symcon_bwd_dA": ops["dA"], "symcon_bwd_dW": ops["dW"],
-                      "symcon_bwd2": ops["bwd2"], "symcon_bwd2_dW": ops["bwd2_dW"]}.get(kern)
-            mean_nodes = nodes / args.steps
-            if per_nc:
-                achieved = per_nc * mean_nodes * K / (avg_ms / 1e3) / 1e12  # T lane-ops/s
-                sm_mhz = 1965.0
-                peak = 148 * 128 * sm_mhz * 1e6 / 1e12
-                nlm = (cfg.lmax_in + 1) ** 2
-                outc = sc.out_dim // K
-                alg_b = {"symcon_fwd": 4 * (nlm + outc), "symcon_bwd_dA": 4 * (2 * nlm + outc),
-                         "symcon_bwd_dW": 4 * (nlm + outc), "symcon_bwd2": 4 * (4 * nlm + 2 * outc),
-                         "symcon_bwd2_dW": 4 * (2 * nlm + outc)}[kern] * mean_nodes * K
-                traffic, tsrc = None, None
-                tpath = os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")
-                if os.path.exists(tpath) and args.config == "mp_medium":
-                    tj = json.load(open(tpath))
-                    rec = tj["kernels"].get(kern)
-                    if rec:
-                        traffic = rec["dram_bytes_read"] + rec["dram_bytes_write"]
-                        tsrc = tj["source"]
-                # the binding resource: ALU time at the FP32 peak vs HBM time at the measured copy
-                # bandwidth, both from the kernel's algorithmic work
-                hbm_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
-                    os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6553.0
-                t_alu = per_nc * mean_nodes * K / (peak * 1e12)
-                t_hbm = alg_b / (hbm_peak * 1e9)
-                if t_hbm > t_alu:
-                    gbs = alg_b / (avg_ms / 1e3) / 1e9
-                    roof = {"bound": "hbm", "kernel": kern, "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
-                            "frac": gbs / hbm_peak, "traffic": traffic, "traffic_source": tsrc,
-                            "algorithmic_bytes": alg_b, "avg_launch_ms": avg_ms, "ops_per_node_channel": per_nc,
-                            "alu_tops": achieved, "alu_frac": achieved / peak,
-                            "peak_derivation": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"}
-                else:
-                    roof = {"bound": "alu", "kernel": kern, "achieved": achieved, "peak": peak,
-                            "unit": "Tops/s (fp32 FMA lane-ops)",
-                            "frac": achieved / peak, "traffic": traffic, "traffic_source": tsrc,
-                            "algorithmic_bytes": alg_b, "avg_launch_ms": avg_ms,
-                            "ops_per_node_channel": per_nc, "hbm_gbs": alg_b / (avg_ms / 1e3) / 1e9,
-                            "peak_derivation": "148 SMs x 128 FP32 lanes x 1965 MHz (clocks.max.sm); FFMA probe measured 36.0 T/s"}
-        path_ops = (ops["path"] + (ops["bwd2"] + ops["bwd2_dW"] if args.double_backward else 0)) * (nodes / args.steps) * K
+        sm_mhz = clocks.get("sm_mhz") or 1965.0
+        peak_alu = 148 * 128 * sm_mhz * 1e6 / 1e12          # T lane-ops/s at the sampled clock
+        mean_nodes = nodes / args.steps
+        roof = kernel_roofline(args, cfg, sc, ops, prof, mean_nodes, peak_alu, sm_mhz)
+        path_ops = (ops["path"] + (ops["bwd2"] + ops["bwd2_dW"] if args.double_backward else 0)) * mean_nodes * K
         kernels = {k: {"launches": v[0], "avg_ms": v[1] / max(v[0], 1)} for k, v in prof.items()}
+        ms_step = ms_max / args.steps
+        ksum = sum(v["avg_ms"] * v["launches"] for v in kernels.values()) / args.steps
+        config = workload_config(args, cfg, pool[0][1])
+        config.update({"bins": ts.shards.n_bins, "global_batch": int(nodes_all / args.steps),
+                       "step_imbalance_max_over_mean": round(ts.imbalance, 5),
+                       "dW_allreduce": ({"peer": f"libsymcon NVLink peer-memory kernel (algo {dp._peer.algo if dp._peer else args.peer_algo}: "
+                                                 "0 auto, 1 one-shot, 2 two-shot), dA concurrent",
+                                         "nccl": "NCCL on a communication stream"}[dp.allreduce] if world > 1 else None),
+                       "seq_len": None, "parallelism": f"dp{world}",
+                       "l2": ("inputs > L2 (A 410 MB/bin), 4-bin pool" if pool[0][1] * K * 64 > 126e6 else
+                              f"4-bin pool of {pool[0][1]}-node bins ({4 * pool[0][1] * K * 80 / 1e6:.0f} MB) fits in L2: "
+                              "no flush (latency-bound regime)"),
+                       "alg1_pack_s": round(ts.t_pack, 3), "cuda_graph": use_graph})
         out = {
-            "metric": "symcon_fwd_bwd_bwd2_nodes_per_s" if args.double_backward else "symcon_fwd_bwd_nodes_per_s", "value": value, "unit": "nodes/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "metric": "symcon_fwd_bwd_bwd2_nodes_per_s" if args.double_backward else "symcon_fwd_bwd_nodes_per_s",
+            "value": value, "unit": "nodes/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.config}_dp_step" + ("_double_backward" if args.double_backward else ""), "model": "MACE symmetric contraction",
-                       "channels": K, "out": "+".join(f"{K}x{L}{'e' if L % 2 == 0 else 'o'}" for L in cfg.out_L),
-                       "lmax_in": cfg.lmax_in, "correlation": cfg.correlation, "elements": cfg.n_elements,
-                       "capacity_nodes": CAPACITY, "bins": n_bins, "global_batch": int(nodes_all / args.steps),
-                       "step_imbalance_max_over_mean": round(imbalance, 5), "dW_allreduce": ({"peer": "libsymcon NVLink peer-memory kernel (symmetric buffers), dA concurrent",
-                                                        "nccl": "NCCL on a communication stream"}[dp.allreduce]
-                                                       if world > 1 else None),
-                       "seq_len": None, "parallelism": f"dp{world}", "l2": "inputs > L2 (A 410 MB/bin), 4-bin pool",
-                       "alg1_pack_s": round(t_pack, 3), "cuda_graph": use_graph},
+            "config": config,
             "per_gpu_nodes_per_s": value / world,
             "per_rank_ms_per_step": per_rank_ms,
-            "path_tops": path_ops / (ms_max / args.steps / 1e3) / 1e12,
-            "path_frac_of_alu_peak": path_ops / (ms_max / args.steps / 1e3) / 1e12 / (148 * 128 * 1.965e-3),
-            "path_roofline": path_roofline(cfg, sc, nodes / args.steps, path_ops, ms_max / args.steps, args.double_backward),
+            "edge_balance": edge_spread(ts.sizes, ts.shards.offsets, ts.shards.ids, world, POOL),
+            "path_tops": path_ops / (ms_step / 1e3) / 1e12,
+            "path_frac_of_alu_peak": path_ops / (ms_step / 1e3) / 1e12 / peak_alu,
+            "path_roofline": path_roofline(cfg, sc, mean_nodes, path_ops, ms_step, args.double_backward, sm_mhz),
             "roofline": roof, "kernels": kernels, "alg_ops_per_node_channel": ops,
+            "step_breakdown_ms": {"step": ms_step, "kernels_back_to_back": ksum,
+                                  "allreduce_alone": ar_ms,
+                                  "note": "kernels_back_to_back = sum of per-launch-group CUDA-event times from the "
+                                          "sequential pass (dW and dA not overlapped); allreduce_alone = one peer "
+                                          "all-reduce call timed alone"},
             "clocks": clocks, "gpu_launches": launches_timed,
             "kernel_timing": "per-kernel CUDA events from a separate pass of the same steps with dW and dA back to back",
             "e2e": {"value": e2e_value, "unit": "nodes/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
@@ -571,11 +652,57 @@ def run_ours(args):
                             "the copy of step s+1 (copy stream) overlaps the compute of step s"},
         }
         if not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline(cfg, sc, A, W, ne, dB, args.cpu_sample)
+            out["cpu_baseline"] = cpu_baseline(cfg, A, W, ne, dB, args.cpu_sample)
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def kernel_roofline(args, cfg, sc, ops, prof, mean_nodes, peak_alu, sm_mhz):
+    """roofline of the dominant kernel (by measured time): its algorithmic ops (or bytes) per launch
+    / its average CUDA-event launch time, against the FP32 peak at the sampled SM clock (or the
+    measured HBM copy bandwidth), whichever binds it."""
+    if not prof:
+        return None
+    kern = max(prof, key=lambda k: prof[k][1])
+    cnt, tot_ms = prof[kern]
+    avg_ms = tot_ms / max(cnt, 1)
+    K = cfg.channels
+    per_nc = {"symcon_fwd": ops["fwd"], "symcon_bwd_dA": ops["dA"], "symcon_bwd_dW": ops["dW"],
+              "symcon_bwd2": ops["bwd2"], "symcon_bwd2_dW": ops["bwd2_dW"]}.get(kern)
+    if not per_nc:
+        return {"kernel": kern, "avg_launch_ms": avg_ms}
+    achieved = per_nc * mean_nodes * K / (avg_ms / 1e3) / 1e12   # T lane-ops/s
+    nlm = (cfg.lmax_in + 1) ** 2
+    outc = sc.out_dim // K
+    alg_b = {"symcon_fwd": 4 * (nlm + outc), "symcon_bwd_dA": 4 * (2 * nlm + outc),
+             "symcon_bwd_dW": 4 * (nlm + outc), "symcon_bwd2": 4 * (4 * nlm + 2 * outc),
+             "symcon_bwd2_dW": 4 * (2 * nlm + outc)}[kern] * mean_nodes * K
+    traffic, tsrc = None, None
+    for tpath in (os.path.join(ROOT, "profiles", "r02", "ncu_traffic.json"),):
+        if os.path.exists(tpath) and args.config == "mp_medium" and args.capacity == CAPACITY:
+            tj = json.load(open(tpath))
+            rec = tj["kernels"].get(kern)
+            if rec:
+                traffic = rec["dram_bytes_read"] + rec["dram_bytes_write"]
+                tsrc = tj["source"]
+    hbm_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6553.0
+    t_alu = per_nc * mean_nodes * K / (peak_alu * 1e12)
+    t_hbm = alg_b / (hbm_peak * 1e9)
+    common = {"kernel": kern, "traffic": traffic, "traffic_source": tsrc, "algorithmic_bytes": alg_b,
+              "avg_launch_ms": avg_ms, "ops_per_node_channel": per_nc}
+    if t_hbm > t_alu:
+        gbs = alg_b / (avg_ms / 1e3) / 1e9
+        return dict(common, bound="hbm", achieved=gbs, peak=hbm_peak, unit="GB/s", frac=gbs / hbm_peak,
+                    alu_tops=achieved, alu_frac=achieved / peak_alu,
+                    peak_derivation="MEASURED_PEAKS.json hbm_gbs (copy bandwidth)")
+    return dict(common, bound="alu", achieved=achieved, peak=peak_alu, unit="Tops/s (fp32 FMA lane-ops)",
+                frac=achieved / peak_alu, hbm_gbs=alg_b / (avg_ms / 1e3) / 1e9,
+                frac_at_max_clock=achieved / (148 * 128 * 1.965e-3),
+                peak_derivation=f"148 SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (median SM clock sampled during the "
+                                "timed region; DESIGN.md §7)")
 
 
 # ----------------------------------------------------------------------------- channelwise TP

@@ -50,7 +50,8 @@ typedef enum {
   SYMCON_EUNSUPPORTED = 2, /* valid but not supported (e.g. correlation > 3) */
   SYMCON_ECUDA = 3,        /* CUDA / NVRTC failure */
   SYMCON_ENOMEM = 4,       /* host allocation or workspace too small */
-  SYMCON_EELEMENT = 5      /* node_elem value outside [0, E) found on the device */
+  SYMCON_EELEMENT = 5,     /* node_elem value outside [0, E) found on the device */
+  SYMCON_ETIMEOUT = 6      /* peer all-reduce: a rank did not reach the barrier (symcon_peer_check) */
 } symcon_status;
 
 typedef struct symcon_plan symcon_plan; /* opaque */
@@ -179,23 +180,47 @@ symcon_status symcon_pack_balanced(const int64_t* sizes, int64_t n, int64_t capa
                                    int32_t workers, int64_t* bin_offsets, int64_t* graph_ids,
                                    int64_t max_bins, int64_t* n_bins);
 
-/* ---- dW all-reduce over NVLink peer memory ----------------
+/* ---- dW all-reduce over NVLink peer memory ("all-reduce") ------
+ * The data-parallel step's one exchange: dW = sum over ranks of each rank's partial.
  * bufs[r] (r < world <= 8): device pointer, valid on this GPU (peer mapping), of rank r's
- * n-float partial; pads[r]: rank r's signal pad (>= world uint32 slots, zero-initialised, peer
- * mapped). One kernel: a cross-GPU barrier (this rank writes `epoch` to slot `rank` of every pad,
- * then waits until all slots of its own pad reach `epoch`; epochs must increase by call), then
- * out[i] = sum_{r = 0..world-1} bufs[r][i] in rank order (bitwise identical on every rank).
+ * n-float partial, 16-byte aligned; pads[r]: rank r's signal pad (>= 2*world + 1 uint32 slots,
+ * zero-initialised, peer mapped; slot 2*world is this rank's private grid counter).
+ * One kernel per call (plus, in the _dev form, a one-thread epoch bump):
+ *   algo 1, one-shot: a cross-GPU barrier (this rank writes `epoch` to slot `rank` of every pad,
+ *     then waits until slots [0, world) of its own pad reach `epoch`; epochs must increase by
+ *     call), then out[i] = sum_{r = 0..world-1} bufs[r][i] in rank order.
+ *   algo 2, two-shot: the same barrier; rank r sums slice r of all partials (rank order) in place
+ *     into slice r of bufs[r]; a second barrier on slots [world, 2 world); out gathers slice q
+ *     from bufs[q]. NVLink reads per rank: 2 (world-1)/world x n floats instead of (world-1) x n.
+ *   algo 0: auto (two-shot for world >= 4).
+ * Every rank ends with bitwise the same out (each element summed once, in rank order).
  * The caller must not overwrite bufs[rank] until every rank's call has completed (alternate two
- * buffers per step). err (device int, may be NULL) is set to 1 if a peer did not arrive within
- * ~seconds (the kernel then returns partial sums instead of hanging). out may alias bufs[rank]
- * only if no peer reads it afterwards. */
+ * buffers per step); with algo 2, bufs[rank] is modified. out must not alias any bufs[r].
+ * Error: a barrier that does not complete within spin_limit polls of ~200 ns (0 = default 2^26,
+ * tens of seconds) is a hard error: *err (device int32, may be NULL) is set to 1 and `out` is
+ * filled with NaN, never with partial sums; symcon_peer_check reports it as SYMCON_ETIMEOUT. */
+symcon_status symcon_peer_allreduce_ex(const float* const* bufs, uint32_t* const* pads, int32_t world, int32_t rank,
+                                       int64_t n, uint32_t epoch, uint32_t* epoch_counter, int32_t algo,
+                                       int64_t spin_limit, float* out, int32_t* err, void* stream);
+/* epoch_counter (nullable): if non-NULL the epoch is read on the device as *epoch_counter + 1 (a
+ * uint32 in device memory, zero-initialised, one per reducer) and the counter is incremented by a
+ * one-thread kernel right after, so a call captured in a CUDA graph can be replayed; `epoch` is
+ * then ignored. */
+/* Legacy forms: one-shot with a host epoch / with a device epoch counter, default spin limit. */
 symcon_status symcon_peer_allreduce(const float* const* bufs, uint32_t* const* pads, int32_t world, int32_t rank,
                                     int64_t n, uint32_t epoch, float* out, int32_t* err, void* stream);
-/* Same, CUDA-graph capturable: the epoch is read on the device from *epoch_counter + 1 (a uint32
- * in device memory, zero-initialised, one per reducer) and the counter is incremented by a
- * one-thread kernel launched right after, so a captured call can be replayed. */
 symcon_status symcon_peer_allreduce_dev(const float* const* bufs, uint32_t* const* pads, int32_t world, int32_t rank,
                                         int64_t n, uint32_t* epoch_counter, float* out, int32_t* err, void* stream);
+/* Diagnostic form for one GPU: the all-reduce of `world` ranks whose buffers (bufs, pads, outs; all
+ * on this device) are all here, run as ONE cooperative launch in which each rank's blocks execute
+ * the same kernel code as symcon_peer_allreduce_ex (rank = blockIdx.y), so the barrier protocol,
+ * the two-shot slices and the rank-order sums are exercised without several GPUs (ranks that wait
+ * on one another must not be separate launches on one GPU). algo 1 or 2. */
+symcon_status symcon_peer_allreduce_emulate(const float* const* bufs, uint32_t* const* pads, float* const* outs,
+                                            int32_t world, int64_t n, uint32_t epoch, int32_t algo, int64_t spin_limit,
+                                            int32_t* err, void* stream);
+/* Synchronises `stream` and reads *err: SYMCON_ETIMEOUT if a barrier of an earlier call timed out. */
+symcon_status symcon_peer_check(const int32_t* err, void* stream);
 
 /* ---- channelwise tensor product + edge->node sum ----------------
  * Alg. 2 of the paper, the message construction that feeds the contraction,

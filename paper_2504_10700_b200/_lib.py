@@ -17,7 +17,7 @@ if not os.path.exists(LIB_PATH):
 
 lib = ctypes.CDLL(LIB_PATH)
 
-SYMCON_OK, SYMCON_EINVAL, SYMCON_EUNSUPPORTED, SYMCON_ECUDA, SYMCON_ENOMEM, SYMCON_EELEMENT = range(6)
+SYMCON_OK, SYMCON_EINVAL, SYMCON_EUNSUPPORTED, SYMCON_ECUDA, SYMCON_ENOMEM, SYMCON_EELEMENT, SYMCON_ETIMEOUT = range(7)
 
 EXPORTS = ["symcon_build_tables", "symcon_plan_info", "symcon_plan_path", "symcon_plan_sym_table", "symcon_real_cg",
            "symcon_workspace_bytes", "symcon_forward", "symcon_backward", "symcon_backward_ex", "symcon_backward2", "symcon_check_device_error",
@@ -26,7 +26,8 @@ EXPORTS = ["symcon_build_tables", "symcon_plan_info", "symcon_plan_path", "symco
            "symcon_profile_reset", "symcon_profile_read", "symcon_tp_build", "symcon_tp_info", "symcon_tp_path",
            "symcon_tp_workspace_bytes", "symcon_tp_forward", "symcon_tp_backward", "symcon_tp_check_device_error",
            "symcon_tp_last_launch_count", "symcon_tp_source", "symcon_tp_destroy", "symcon_peer_allreduce",
-           "symcon_tp_precompile", "symcon_peer_allreduce_dev"]
+           "symcon_tp_precompile", "symcon_peer_allreduce_dev", "symcon_peer_allreduce_ex", "symcon_peer_check",
+           "symcon_peer_allreduce_emulate"]
 
 
 class SymconInfo(ctypes.Structure):
@@ -314,3 +315,35 @@ def symcon_peer_allreduce_dev(bufs, pads, rank, n, epoch_counter, out, err, stre
     p = (_vp * world)(*pads)
     check(lib.symcon_peer_allreduce_dev(b, p, world, rank, n, epoch_counter, out, err, stream),
           "symcon_peer_allreduce_dev")
+
+
+lib.symcon_peer_allreduce_ex.argtypes = [_vp, _vp, _i32, _i32, _i64, ctypes.c_uint32, _vp, _i32, _i64, _vp, _vp, _vp]
+lib.symcon_peer_allreduce_ex.restype = ctypes.c_int
+
+
+def symcon_peer_allreduce_ex(bufs, pads, rank, n, epoch, epoch_counter, algo, spin_limit, out, err, stream):
+    world = len(bufs)
+    b = (_vp * world)(*bufs)
+    p = (_vp * world)(*pads)
+    check(lib.symcon_peer_allreduce_ex(b, p, world, rank, n, epoch, epoch_counter, algo, spin_limit, out, err, stream),
+          "symcon_peer_allreduce_ex")
+
+
+lib.symcon_peer_check.argtypes = [_vp, _vp]
+lib.symcon_peer_check.restype = ctypes.c_int
+
+
+def symcon_peer_check(err, stream):
+    """Synchronises; raises SymconError(SYMCON_ETIMEOUT) if an all-reduce barrier timed out."""
+    check(lib.symcon_peer_check(err, stream), "symcon_peer_check")
+
+
+lib.symcon_peer_allreduce_emulate.argtypes = [_vp, _vp, _vp, _i32, _i64, ctypes.c_uint32, _i32, _i64, _vp, _vp]
+lib.symcon_peer_allreduce_emulate.restype = ctypes.c_int
+
+
+def symcon_peer_allreduce_emulate(bufs, pads, outs, n, epoch, algo, spin_limit, err, stream):
+    world = len(bufs)
+    b, p, o = (_vp * world)(*bufs), (_vp * world)(*pads), (_vp * world)(*outs)
+    check(lib.symcon_peer_allreduce_emulate(b, p, o, world, n, epoch, algo, spin_limit, err, stream),
+          "symcon_peer_allreduce_emulate")

@@ -273,6 +273,7 @@ const char* symcon_status_string(symcon_status s) {
     case SYMCON_ECUDA: return "CUDA error";
     case SYMCON_ENOMEM: return "out of memory / workspace too small";
     case SYMCON_EELEMENT: return "node_elem out of range (species index without weights)";
+    case SYMCON_ETIMEOUT: return "peer all-reduce barrier timed out";
   }
   return "unknown";
 }
@@ -738,43 +739,95 @@ symcon_status symcon_backward2(const symcon_plan* p, int64_t N, const float* A, 
 }
 
 static symcon_status peer_common(const float* const* bufs, uint32_t* const* pads, int32_t world, int32_t rank,
-                                 int64_t n, uint32_t epoch, uint32_t* epoch_dev, float* out, int32_t* err, void* stream);
+                                 int64_t n, uint32_t epoch, uint32_t* epoch_dev, int32_t algo, int64_t spin_limit,
+                                 float* out, int32_t* err, void* stream);
 
 symcon_status symcon_peer_allreduce(const float* const* bufs, uint32_t* const* pads, int32_t world, int32_t rank,
                                     int64_t n, uint32_t epoch, float* out, int32_t* err, void* stream) {
-  return peer_common(bufs, pads, world, rank, n, epoch, nullptr, out, err, stream);
+  return peer_common(bufs, pads, world, rank, n, epoch, nullptr, 1, 0, out, err, stream);
 }
 
 symcon_status symcon_peer_allreduce_dev(const float* const* bufs, uint32_t* const* pads, int32_t world, int32_t rank,
                                         int64_t n, uint32_t* epoch_counter, float* out, int32_t* err, void* stream) {
   if (!epoch_counter) { set_error("NULL epoch counter"); return SYMCON_EINVAL; }
-  return peer_common(bufs, pads, world, rank, n, 0, epoch_counter, out, err, stream);
+  return peer_common(bufs, pads, world, rank, n, 0, epoch_counter, 1, 0, out, err, stream);
+}
+
+symcon_status symcon_peer_allreduce_ex(const float* const* bufs, uint32_t* const* pads, int32_t world, int32_t rank,
+                                       int64_t n, uint32_t epoch, uint32_t* epoch_counter, int32_t algo,
+                                       int64_t spin_limit, float* out, int32_t* err, void* stream) {
+  if (algo < 0 || algo > 2) { set_error("algo must be 0 (auto), 1 (one-shot) or 2 (two-shot)"); return SYMCON_EINVAL; }
+  if (spin_limit < 0) { set_error("spin_limit must be >= 0"); return SYMCON_EINVAL; }
+  if (algo == 0) algo = world >= 4 ? 2 : 1;
+  return peer_common(bufs, pads, world, rank, n, epoch, epoch_counter, algo, spin_limit, out, err, stream);
+}
+
+symcon_status symcon_peer_check(const int32_t* err, void* stream) {
+  if (!err) { set_error("NULL err"); return SYMCON_EINVAL; }
+  symcon_status s = cuda_err(cudaStreamSynchronize((cudaStream_t)stream), "stream sync");
+  if (s) return s;
+  int32_t e = 0;
+  s = cuda_err(cudaMemcpy(&e, err, sizeof e, cudaMemcpyDeviceToHost), "read all-reduce error word");
+  if (s) return s;
+  if (e) { set_error("peer all-reduce barrier timed out: a rank did not arrive (output set to NaN)"); return SYMCON_ETIMEOUT; }
+  return SYMCON_OK;
 }
 
 static symcon_status peer_common(const float* const* bufs, uint32_t* const* pads, int32_t world, int32_t rank,
-                                 int64_t n, uint32_t epoch, uint32_t* epoch_dev, float* out, int32_t* err, void* stream) {
+                                 int64_t n, uint32_t epoch, uint32_t* epoch_dev, int32_t algo, int64_t spin_limit,
+                                 float* out, int32_t* err, void* stream) {
   if (!bufs || !pads || !out || world < 1 || world > 8 || rank < 0 || rank >= world || n < 0) {
     set_error("bad peer all-reduce arguments");
     return SYMCON_EINVAL;
   }
+  if (!aligned16(out)) { set_error("out must be 16-byte aligned"); return SYMCON_EINVAL; }
   PeerArgs a{};
   for (int r = 0; r < world; r++) {
     if (!bufs[r] || !pads[r]) { set_error("NULL peer pointer"); return SYMCON_EINVAL; }
+    if (!aligned16(bufs[r])) { set_error("peer buffers must be 16-byte aligned"); return SYMCON_EINVAL; }
     a.buf[r] = bufs[r];
     a.pad[r] = pads[r];
   }
-  static int* dummy_err = nullptr;
-  if (!err) {
-    if (!dummy_err) cudaMalloc(&dummy_err, sizeof(int));
-    err = dummy_err;
-  }
+  // default ~2^26 polls of ~200 ns: tens of seconds (a rank checkpointing or evaluating must not
+  // trip it; a dead rank still ends in a reported error instead of a hang)
+  const long long limit = spin_limit > 0 ? (long long)spin_limit : (1ll << 26);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long n4 = (n + 3) / 4;
+  a.out[rank] = out;
   const int blocks = (int)std::max<long long>(1, std::min<long long>(sms, (n4 + 511) / 512));
-  peer_allreduce_launch(a, world, rank, n, epoch, epoch_dev, out, err, blocks, (cudaStream_t)stream);
+  peer_allreduce_launch(a, world, rank, n, epoch, epoch_dev, algo, limit, err, blocks, (cudaStream_t)stream);
   return cuda_err(cudaGetLastError(), "peer all-reduce launch");
+}
+
+symcon_status symcon_peer_allreduce_emulate(const float* const* bufs, uint32_t* const* pads, float* const* outs,
+                                            int32_t world, int64_t n, uint32_t epoch, int32_t algo, int64_t spin_limit,
+                                            int32_t* err, void* stream) {
+  if (!bufs || !pads || !outs || world < 1 || world > 8 || n < 0 || algo < 1 || algo > 2) {
+    set_error("bad emulated all-reduce arguments");
+    return SYMCON_EINVAL;
+  }
+  PeerArgs a{};
+  for (int r = 0; r < world; r++) {
+    if (!bufs[r] || !pads[r] || !outs[r] || !aligned16(bufs[r]) || !aligned16(outs[r])) {
+      set_error("NULL or misaligned buffer");
+      return SYMCON_EINVAL;
+    }
+    a.buf[r] = bufs[r];
+    a.pad[r] = pads[r];
+    a.out[r] = outs[r];
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // all world x blocks CTAs of 512 threads must be co-resident (at most 2 per SM here)
+  const long long n4 = (n + 3) / 4;
+  const int blocks = (int)std::max<long long>(1, std::min<long long>(std::min(sms, std::max(1, 2 * sms / world)), (n4 + 511) / 512));
+  const long long limit = spin_limit > 0 ? (long long)spin_limit : (1ll << 26);
+  if (peer_allreduce_launch(a, world, -1, n, epoch, nullptr, algo, limit, err, blocks, (cudaStream_t)stream) < 0)
+    return cuda_err(cudaGetLastError(), "cooperative launch of the emulated all-reduce");
+  return cuda_err(cudaGetLastError(), "emulated all-reduce launch");
 }
 
 symcon_status symcon_check_device_error(const symcon_plan* p, void* ws, void* stream, int64_t* first_bad) {

@@ -34,9 +34,13 @@ int reduce_items_launch(const float* spart, const int* item_off, int E, int npad
 struct PeerArgs {
   const float* buf[8];   // each rank's symmetric dW buffer (peer pointers)
   unsigned* pad[8];      // each rank's signal pad (uint32 flags, slot r written by rank r)
+  float* out[8];         // output of rank r (only out[rank] is used unless emulating)
 };
+// algo 1 one-shot, 2 two-shot (reduce-scatter + all-gather); spin_limit = barrier polls before
+// the hard timeout (err = 1, NaN output); rank < 0 emulates all ranks on this device in one
+// cooperative launch (blocks per rank x world). Returns launches issued, -1 on launch failure.
 int peer_allreduce_launch(const PeerArgs& a, int world, int rank, long long n, unsigned epoch, unsigned* epoch_dev,
-                          float* out, int* err, int blocks, cudaStream_t st);
+                          int algo, long long spin_limit, int* err, int blocks, cudaStream_t st);
 
 // channelwise TP (tp_static.cu)
 struct TPCsrArgs {

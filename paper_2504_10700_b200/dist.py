@@ -50,42 +50,43 @@ class BinPackedShards:
 
 class PeerReducer:
     """Two symmetric (peer-mapped) fp32 buffers used alternately per step + one signal pad; the
-    all-reduce itself is libsymcon's kernel (no NCCL)."""
+    all-reduce itself is libsymcon's kernel (no NCCL). algo: 0 auto (two-shot for world >= 4),
+    1 one-shot, 2 two-shot (symcon_peer_allreduce_ex). A barrier timeout is a hard error: the
+    kernel writes NaN and sets `err`; `check()` raises it (SYMCON_ETIMEOUT)."""
 
-    def __init__(self, numel, device, group=None):
+    def __init__(self, numel, device, group=None, algo=0, spin_limit=0):
         import torch.distributed._symmetric_memory as symm
         grp = group if group is not None else dist.group.WORLD
-        import warnings
-        try:
-            with warnings.catch_warnings():
-                warnings.simplefilter("ignore")
-                symm.enable_symm_mem_for_group(grp.group_name)
-        except Exception:  # noqa: BLE001  (newer torch: not needed)
-            pass
         self.numel = int(numel)
+        self.algo, self.spin_limit = int(algo), int(spin_limit)
         self.bufs = [symm.empty(self.numel, dtype=torch.float32, device=device) for _ in range(2)]
         self.hdl = [symm.rendezvous(b, grp) for b in self.bufs]
         self.rank, self.world = self.hdl[0].rank, self.hdl[0].world_size
-        pad = self.hdl[0].get_signal_pad(self.rank, (self.world,), dtype=torch.int32)
+        # slots [0, world): first barrier, [world, 2 world): two-shot second barrier, 2 world: grid counter
+        pad = self.hdl[0].get_signal_pad(self.rank, (2 * self.world + 1,), dtype=torch.int32)
         pad.zero_()
         self.err = torch.zeros(1, dtype=torch.int32, device=device)
         self.counter = torch.zeros(1, dtype=torch.int32, device=device)   # device epoch (graph-capturable)
         torch.cuda.synchronize(device)
         dist.barrier(group=group)
-        self.epoch = 0
         self.parity = 0
 
     def buffer(self):
         return self.bufs[self.parity]
 
     def allreduce(self, out, stream):
-        """Epoch kept on the device (symcon_peer_allreduce_dev), so the call can be captured in a
-        CUDA graph; the buffer parity alternates per call (capture an even number of steps)."""
+        """Epoch kept on the device, so the call can be captured in a CUDA graph; the buffer parity
+        alternates per call (capture an even number of steps)."""
         h = self.hdl[self.parity]
-        _lib.symcon_peer_allreduce_dev(list(h.buffer_ptrs), list(self.hdl[0].signal_pad_ptrs), self.rank, self.numel,
-                                       self.counter.data_ptr(), out.data_ptr(), self.err.data_ptr(), stream)
+        _lib.symcon_peer_allreduce_ex(list(h.buffer_ptrs), list(self.hdl[0].signal_pad_ptrs), self.rank, self.numel, 0,
+                                      self.counter.data_ptr(), self.algo, self.spin_limit, out.data_ptr(),
+                                      self.err.data_ptr(), stream)
         self.parity ^= 1
         return out
+
+    def check(self):
+        """Synchronises; raises SymconError (SYMCON_ETIMEOUT) if a barrier of an earlier call timed out."""
+        _lib.symcon_peer_check(self.err.data_ptr(), torch.cuda.current_stream(self.err.device).cuda_stream)
 
 
 class DataParallelContraction:
@@ -93,12 +94,14 @@ class DataParallelContraction:
     kernel on a side stream (concurrently; `concurrent_bwd`), and for N > 1 the dW all-reduce
     runs on a communication stream as soon as dW is ready, overlapped with dA."""
 
-    def __init__(self, sc, group=None, overlap=True, concurrent_bwd=None, allreduce=None):
+    def __init__(self, sc, group=None, overlap=True, concurrent_bwd=None, allreduce=None, peer_algo=0):
         self.sc = sc
         self.group = group
         self.overlap = overlap
         self.allreduce = allreduce or "peer"
+        self.peer_algo = int(peer_algo)
         self._peer = None
+        self._peer2 = None
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         # measured (profiles/r01): dA concurrent with dW helps at N=1 (+2-4%) and is the default at
         # every N (the dW all-reduce then runs as SMs free up)
@@ -106,6 +109,13 @@ class DataParallelContraction:
         self.side = torch.cuda.Stream(device=sc.device) if self.concurrent_bwd else None
         self.comm = torch.cuda.Stream(device=sc.device) if self.world > 1 else None
         self.launches = 0
+
+    def check(self):
+        """Synchronises; raises if a peer all-reduce barrier of an earlier step timed out (the
+        kernel then wrote NaN into dW / W_bar instead of partial sums)."""
+        for r in (self._peer, getattr(self, "_peer2", None)):
+            if r is not None:
+                r.check()
 
     def forward(self, A, W, node_elem, B=None):
         B = self.sc.forward_raw(A, W, node_elem, B=B)
@@ -132,7 +142,7 @@ class DataParallelContraction:
         main = torch.cuda.current_stream(sc.device)
         if self.allreduce == "peer" and self._peer is None:
             try:
-                self._peer = PeerReducer(W.numel(), sc.device, self.group)
+                self._peer = PeerReducer(W.numel(), sc.device, self.group, algo=self.peer_algo)
             except Exception as exc:  # noqa: BLE001  (no symmetric memory on this system: NCCL)
                 import sys
                 print(f"[symcon] peer-memory all-reduce unavailable ({exc!r}); using NCCL", file=sys.stderr)
@@ -140,16 +150,22 @@ class DataParallelContraction:
         if self.allreduce == "peer":
             if dW is None:
                 dW = torch.empty_like(W)
-            self.side.wait_stream(main)
+            if self.side is not None:
+                self.side.wait_stream(main)
             part = self._peer.buffer()[:W.numel()].view(W.shape)
             sc.backward_raw(A, W, node_elem, dB, need_dA=False, dW=part, reuse=True)
             self.launches += sc.last_launch_count()
-            with torch.cuda.stream(self.side):
+            if self.side is not None:
+                with torch.cuda.stream(self.side):
+                    dA, _ = sc.backward_raw(A, W, node_elem, dB, need_dW=False, dA=dA, reuse=True)
+                    self.launches += sc.last_launch_count()
+            self._peer.allreduce(dW, main.cuda_stream)
+            self.launches += 2
+            if self.side is not None:
+                main.wait_stream(self.side)
+            else:
                 dA, _ = sc.backward_raw(A, W, node_elem, dB, need_dW=False, dA=dA, reuse=True)
                 self.launches += sc.last_launch_count()
-            self._peer.allreduce(dW, main.cuda_stream)
-            self.launches += 1
-            main.wait_stream(self.side)
             return dA, dW
         if not self.overlap:
             dA, dW = sc.backward_raw(A, W, node_elem, dB, dA=dA, dW=dW, reuse=True)
@@ -188,28 +204,31 @@ class DataParallelContraction:
             self.launches += sc.last_launch_count()
             return out
         main = torch.cuda.current_stream(sc.device)
-        if self.allreduce == "peer" and getattr(self, "_peer2", None) is None:
+        if self.allreduce == "peer" and self._peer2 is None:
             try:
-                self._peer2 = PeerReducer(W.numel(), sc.device, self.group)
+                self._peer2 = PeerReducer(W.numel(), sc.device, self.group, algo=self.peer_algo)
             except Exception as exc:  # noqa: BLE001
                 import sys
                 print(f"[symcon] peer-memory all-reduce unavailable ({exc!r}); using NCCL", file=sys.stderr)
                 self.allreduce = "nccl"
         if self.allreduce == "peer":
             part = self._peer2.buffer()[:W.numel()].view(W.shape)
-            self.side.wait_stream(main)
+            side = self.side if self.side is not None else main
+            if side is not main:
+                side.wait_stream(main)
             # W_bar partial straight into the symmetric buffer (main), the tile part on the side stream
             sc.backward2_raw(A, W, node_elem, dB, uA, False, False, True, reuse=True, W_bar=part)
             self.launches += sc.last_launch_count()
             dBb = Ab = None
             if need_dB or need_A:
-                with torch.cuda.stream(self.side):
+                with torch.cuda.stream(side):
                     dBb, Ab, _ = sc.backward2_raw(A, W, node_elem, dB, uA, need_dB, need_A, False, reuse=True)
                     self.launches += sc.last_launch_count()
             Wb = torch.empty_like(W)
             self._peer2.allreduce(Wb, main.cuda_stream)
-            self.launches += 1
-            main.wait_stream(self.side)
+            self.launches += 2
+            if side is not main:
+                main.wait_stream(side)
             return dBb, Ab, Wb
         _, _, Wb = sc.backward2_raw(A, W, node_elem, dB, uA, False, False, True, reuse=True)
         self.launches += sc.last_launch_count()

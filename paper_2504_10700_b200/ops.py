@@ -133,8 +133,9 @@ class _SymconFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, A, W, node_elem, sc):
         ctx.sc = sc
-        ctx.save_for_backward(A, W, node_elem)
-        return sc.forward_raw(A.contiguous(), W.contiguous(), node_elem.contiguous())
+        A, W, node_elem = A.contiguous(), W.contiguous(), node_elem.contiguous()
+        ctx.save_for_backward(A, W, node_elem)   # the contiguous tensors the kernels ran on
+        return sc.forward_raw(A, W, node_elem)
 
     @staticmethod
     def backward(ctx, dB):

@@ -1,9 +1,10 @@
 """Seeded input generators (SURVEY.md §8(d) "Synthetic inputs").
 
 Seeds: A=1, W=2, node_elem=3, dB=4, graph sizes=5 (each offset by `seed`).
-Tensors are generated with torch generators on the requested device so the
-full-size configs can be made directly in HBM; small configs are compared with
-the oracle by copying the very same tensors to the host.
+A, W and dB are drawn by a CPU torch generator and then moved to the requested
+device, so a seed gives the same values on every device: the GPU arm of bench.py
+and the oracle (reference arm, parity tests) see identical inputs. The TP inputs
+(several GB per bin) are drawn on the requested device.
 """
 from dataclasses import dataclass
 import math
@@ -87,24 +88,31 @@ def gen_node_elem(n_nodes, n_elements, dist="uniform", device="cpu", seed=0):
 
 
 def gen_A(n_nodes, channels, n_lm=16, device="cpu", seed=0):
-    g = _gen(device, 1 + seed)
-    return torch.randn((n_nodes, channels, n_lm), generator=g, device=device, dtype=torch.float32)
+    g = _gen("cpu", 1 + seed)
+    return torch.randn((n_nodes, channels, n_lm), generator=g, dtype=torch.float32).to(device)
 
 
 def gen_W(n_elements, block_sizes, channels, device="cpu", seed=0):
     """W [E][P][K] ~ N(0,1)/n_eta per (L, nu) block (MACE-style init; unpinned).
 
     block_sizes: [(L, nu, n_eta)] in W column order (the caller supplies it)."""
-    g = _gen(device, 2 + seed)
+    g = _gen("cpu", 2 + seed)
     P = sum(b[2] for b in block_sizes)
-    W = torch.randn((n_elements, P, channels), generator=g, device=device, dtype=torch.float32)
-    scale = torch.cat([torch.full((b[2],), 1.0 / b[2]) for b in block_sizes]).to(device)
-    return W * scale.view(1, P, 1)
+    W = torch.randn((n_elements, P, channels), generator=g, dtype=torch.float32)
+    scale = torch.cat([torch.full((b[2],), 1.0 / b[2]) for b in block_sizes])
+    return (W * scale.view(1, P, 1)).to(device)
 
 
 def gen_dB(n_nodes, out_dim, device="cpu", seed=0):
-    g = _gen(device, 4 + seed)
-    return torch.randn((n_nodes, out_dim), generator=g, device=device, dtype=torch.float32)
+    g = _gen("cpu", 4 + seed)
+    return torch.randn((n_nodes, out_dim), generator=g, dtype=torch.float32).to(device)
+
+
+def graph_edges(sizes, deg=30):
+    """Edges of graphs of the given vertex counts under the synthetic degree min(deg, n-1) per node
+     -- the secondary load key of the DP step."""
+    sizes = np.asarray(sizes, dtype=np.int64)
+    return sizes * np.minimum(deg, np.maximum(sizes - 1, 0))
 
 
 def molecule_sizes(total, lo=10, hi=100, seed=0):

@@ -35,6 +35,22 @@ def test_properties_random(seed):
     assert eq3_max_gap(bins, sizes) >= 0
 
 
+def test_eq2_eq3_hand_trace_values():
+    """Eq. (2) and Eq. (3) on the hand-traced Alg. 1 plan of
+    tests/golden/alg1_hand_trace.json, worked by hand (W = C = 8):
+      Eq. (2) = (7^2 + 5^2 + 4^2 + 3^2 + 2^2 + 1^2) / 8^2 = 104 / 64 = 1.625
+      Eq. (3): squared loads per bin {7}->49, {5}->25, {4,1}->17, {3,2}->13; max gap 49 - 13 = 36.
+    A dropped square (Eq. 2 -> 22/64, Eq. 3 -> 7 - 5 = 2), a missing /W^2 or a max-only Eq. (3)
+    fails here."""
+    g = json.load(open(os.path.join(GOLD, "alg1_hand_trace.json")))
+    bins = create_balanced_batches(g["sizes"], g["capacity"], g["gpus"])
+    assert eq2_padding(bins, g["sizes"], g["capacity"]) == 1.625
+    assert eq3_max_gap(bins, g["sizes"]) == 36
+    # a worse plan of the same graphs has a larger Eq. (3) gap: {7,1} {5,3} {4,2} {} -> 50, 34, 20, 0
+    assert eq3_max_gap([[0, 5], [1, 3], [2, 4], []], g["sizes"]) == 50
+    assert eq1_num_bins([[0, 5], [1, 3], [2, 4], []]) == 3
+
+
 def test_oversize_rejected_and_empty():
     with pytest.raises(ValueError):
         create_balanced_batches([5, 9], 8, 2)
