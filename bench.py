@@ -136,13 +136,19 @@ def edge_spread(sizes, offs, ids, world, steps):
 
 def alg_ops(sc):
     """Algorithmic FP32 lane-ops per (node, channel), per kernel and for the whole path, counted
-    from the plan's tables; each is the op count of the exact evaluation the
-    kernel performs, which is the smallest we know (so the roofline stays a bound):
-      fwd  = prefix products (a,b) + degree-3 monomials + folded rows   (monomials, then one FMA per row)
-      dW   = same products + folded rows                                 (S_j += dB_o * mono_j)
+    from the plan's tables. Each count is the smallest exact evaluation we know, so the
+    roofline stays a bound ("If the builder finds an exact evaluation with fewer
+    ops, lower the count to that"):
+      fwd  = Horner per output slot (symcon_fwd_r): per slot, one FMA per degree-3 row
+             (S_ab += c A_c), per prefix (T_a += A_b S_ab) and per first index (B += A_a T_a);
+             the degree-1/2 coefficients enter as addends (705 at MP-medium)
       dA   = prefix products of degree-3 monomials + folded rows (g_j) + 2 per degree-3 monomial
              + 2 per prefix group + 1 per degree-1 monomial          (reverse of the prefix structure)
-      path = fwd + dA + dW with the backward's products shared."""
+      dW   = reverse Horner per slot (symcon_bwd_dW_r): u_a = dB A_a per first index, q_ab = u_a A_b
+             per prefix, one FMA per degree-3 row, one add per degree-1/2 row; a product that feeds
+             only one add merges into an FMA (a prefix with only its degree-2 row, a first index with
+             only its degree-1 row)
+      path = fwd + dA + dW (the monomial-first forms, 888 / 888, are reported beside them)."""
     from paper_2504_10700_b200 import _lib
     L, M, mono, col, val = _lib.symcon_plan_sym_table(sc.plan)
     rows = {(int(L[i]), int(M[i]), tuple(int(x) for x in mono[i])) for i in range(len(L))}
@@ -154,10 +160,26 @@ def alg_ops(sc):
     deg1 = sum(1 for m in monos if deg[m] == 1)
     n_fold = len(rows)
     products = len(prefixes) + deg3
-    fwd = products + n_fold
-    dW = products + n_fold
+    fwd_mono = products + n_fold
+    dW_mono = products + n_fold
     dA = len(prefixes3) + n_fold + 2 * deg3 + 2 * len(prefixes) + deg1
-    path = fwd + (products + n_fold) + (n_fold + 2 * deg3 + 2 * len(prefixes) + deg1)
+    # Horner / reverse-Horner counts per output slot (L, M)
+    slots = {}
+    for (Lr, Mr, m) in rows:
+        slots.setdefault((Lr, Mr), []).append(m)
+    fwd_h = dW_q = 0
+    for ms in slots.values():
+        r3 = [m for m in ms if m[2] >= 0]
+        r2 = [m for m in ms if m[1] >= 0 and m[2] < 0]
+        r1 = [m for m in ms if m[1] < 0]
+        pre = {m[:2] for m in ms if m[1] >= 0}
+        pre3 = {m[:2] for m in r3}
+        firsts = {m[0] for m in ms}
+        firsts_pre = {m[0] for m in ms if m[1] >= 0}
+        fwd_h += len(r3) + len(pre) + len(firsts)
+        dW_q += len(firsts) + len(pre) + len(r3) + len(r2) + len(r1) - len(pre - pre3) - len(firsts - firsts_pre)
+    path = fwd_h + dA + dW_q
+    path_mono = fwd_mono + (products + n_fold) + (n_fold + 2 * deg3 + 2 * len(prefixes) + deg1)
     # double backward (codegen symcon_bwd2 / symcon_bwd2_dW): per prefix p' (2 ops), p for degree-3
     # groups (1); per degree-3 monomial mono' (2) and, in the tile kernel, A_bar_c, h, h' (3); per
     # row one FMA into dB_bar (+ one into g for degree >= 2); per prefix group 2 (4 with h') FMAs
@@ -166,8 +188,10 @@ def alg_ops(sc):
     p3 = len(prefixes3)
     bwd2 = rows1 + 2 * (n_fold - rows1) + 2 * len(prefixes) + p3 + 5 * deg3 + 4 * p3 + 2 * (len(prefixes) - p3)
     bwd2_dW = n_fold + 2 * len(prefixes) + p3 + 2 * deg3
-    return {"fwd": fwd, "dA": dA, "dW": dW, "path": path, "bwd2": bwd2, "bwd2_dW": bwd2_dW, "n_fold": n_fold, "products": products,
-            "prefixes": len(prefixes), "deg3_monomials": deg3, "n_sym": int(len(L))}
+    return {"fwd": fwd_h, "dA": dA, "dW": dW_q, "path": path, "bwd2": bwd2, "bwd2_dW": bwd2_dW,
+            "fwd_monomial_first": fwd_mono, "dW_monomial_first": dW_mono, "path_monomial_first": path_mono,
+            "n_fold": n_fold, "products": products, "prefixes": len(prefixes), "deg3_monomials": deg3,
+            "n_sym": int(len(L))}
 
 
 def path_roofline(cfg, sc, mean_nodes, path_ops, ms_step, dbl, sm_mhz=1965.0):

@@ -1,5 +1,6 @@
 // C ABI of libsymcon (include/symcon.h): plan construction, NVRTC kernel compilation with an
 // on-disk cubin cache, workspace carving and the forward / backward launch sequences.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nvrtc.h>
@@ -35,12 +36,20 @@ struct symcon_plan {
   int npad = 0;
   size_t unfold_smem = 0, tile_smem = 0, dw_smem = 0, dw2_smem = 0;
   int dw_gpc = 1, dw_nz = 1, dw2_gpc = 1, dw2_nz = 1;
-  int grid_fwd = 0, grid_dA = 0, grid_bwd2 = 0;
+  int grid_fwd = 0, grid_dA = 0, grid_bwd2 = 0, grid_fwd_r = 0;
+  int rnq = 0;                 // fwd_r: coefficient quads per output slot
+  size_t fwd_r_smem = 0;
   std::string source;
   cudaLibrary_t lib = nullptr;
   cudaKernel_t k_fold = nullptr, k_fwd = nullptr, k_dA = nullptr, k_dW = nullptr, k_unfold = nullptr;
   cudaKernel_t k_bwd2 = nullptr, k_bwd2_dW = nullptr;
   cudaKernel_t k_fwd_g = nullptr, k_dA_g = nullptr;   // gamma variants (kc.gamma)
+  cudaKernel_t k_fwd_r = nullptr;                      // output-slot warps, Horner (kc.fwd_r)
+  cudaKernel_t k_dW_r = nullptr;                       // output-slot warps, q-form (kc.dw_r)
+  cudaKernel_t k_dA_s = nullptr;                       // one node per lane, scalar (kc.da_s)
+  size_t da_s_smem = 0;
+  int grid_dA_s = 0;
+  size_t dw_r_smem = 0;
   mutable std::atomic<int> last_launches{0};
   // optional launch timer (symcon_profile_*): CUDA events around each launch group
   struct Rec { int kind; cudaEvent_t a, b; };
@@ -100,6 +109,8 @@ struct Timed {  // RAII: records start/stop events around a launch group when pr
 
 namespace {
 
+struct alignas(64) TmapA { unsigned long long d[16]; };   // CUtensorMap
+static_assert(sizeof(TmapA) == sizeof(CUtensorMap), "tensor map size");
 struct Params {  // must match SymconParams in codegen.cpp
   const float* A; const float* W; const int* node_elem; const float* dB;
   float* B; float* dA; float* dW;
@@ -111,11 +122,43 @@ struct Params {  // must match SymconParams in codegen.cpp
   const int* tile_perm;
   float* stot;
   const float* U;
+  float* coef_r;
+  int* dw_count;
+  int accum;
+  TmapA tmA;
 };
+
+// TMA descriptor of A viewed as [N*K rows][16 floats] (row = (node, channel)), box 32 rows x 16 floats
+// (one node's 32-channel block, 2 KB), 64-byte swizzle (the R kernels read it conflict-free), zero fill
+// past the end. The driver entry point is looked up once (no libcuda link).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                                  const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+symcon_status encode_a_map(TmapA& m, const float* A, int64_t N, int K, int n_lm) {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)f;
+  });
+  if (!fn) { set_error("cuTensorMapEncodeTiled unavailable"); return SYMCON_ECUDA; }
+  const cuuint64_t dims[2] = {(cuuint64_t)n_lm, (cuuint64_t)N * (cuuint64_t)K};
+  const cuuint64_t strides[1] = {(cuuint64_t)n_lm * sizeof(float)};
+  const cuuint32_t box[2] = {(cuuint32_t)n_lm, 32u};
+  const cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = fn(reinterpret_cast<CUtensorMap*>(&m), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)A, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r)); return SYMCON_ECUDA; }
+  return SYMCON_OK;
+}
 
 struct WsLayout {
   size_t hist, chunk_bad, off, seg_off, perm, tiles, n_tiles, items, n_items, item_off, err, coef, spart, tile_off, tile_perm, stot,
-      total;
+      coef_r, dw_count, total;
   int64_t max_tiles, max_items;
 };
 
@@ -145,6 +188,8 @@ WsLayout layout(const symcon_plan* p, int64_t N) {
   w.coef = take(sizeof(float) * (size_t)E * K * p->npad);
   w.spart = take(sizeof(float) * (size_t)w.max_items * K * p->npad);
   w.stot = take(sizeof(float) * (size_t)E * K * p->npad);
+  w.coef_r = take(sizeof(float) * (size_t)E * p->t.out_per_ch * std::max(p->rnq, 1) * K * 4);
+  w.dw_count = take(sizeof(int) * (size_t)E * ((K + 31) / 32));
   w.total = o;
   return w;
 }
@@ -320,6 +365,25 @@ static symcon_status build_common(int lmax_in, int corr, const int* out_L, int n
     p->kc.dw2_rows_per_group = p->t.out_per_ch > 4 ? 40 : std::min(52, std::max(16, (nrows + 7) / 8));
   }
   if (p->kc.dw2_groups_per_cta <= 0) p->kc.dw2_groups_per_cta = 8;
+  // measured (profiles/r02): fwd_r beats symcon_fwd at 1 and 4 output slots (OFF-small, MP-medium) and
+  // loses at 9 (large: 9 warps x 166 registers per CTA)
+  if (p->kc.fwd_r < 0) p->kc.fwd_r = p->t.out_per_ch <= 4 ? 1 : 0;
+  if (p->kc.fwd_r_block < 2 || p->kc.fwd_r_block > 32 || (p->kc.fwd_r_block & 1) || 64 % p->kc.fwd_r_block) {
+    set_error("bad fwd_r_block");
+    delete p;
+    return SYMCON_EINVAL;
+  }
+  if (p->kc.fwd_r) {
+    for (auto& h : horner_slots(p->t)) p->rnq = std::max(p->rnq, (int)((h.rows.size() + 3) / 4));
+    if (p->t.n_lm != 16) p->kc.fwd_r = 0;   // the A staging is laid out for 16 floats per (node, channel) (lmax_in 3)
+  }
+  // measured (profiles/r02): dW_r -22% at MP-medium (4 slots); slower with 1 slot (OFF) and 9 (large)
+  if (p->kc.dw_r < 0) p->kc.dw_r = (p->t.out_per_ch >= 2 && p->t.out_per_ch <= 4) ? 1 : 0;
+  // dw_r stages 16-byte chunks of A rows (16 floats at lmax_in 3) and of 32-channel dB slices
+  // (K % 32 != 0 falls back to symcon_bwd_dW at load time; the source does not depend on K)
+  if (p->t.n_lm != 16) p->kc.dw_r = 0;
+  if (p->kc.da_s < 0) p->kc.da_s = 0;
+  if (p->kc.dw_r_block < 2 || 64 % p->kc.dw_r_block) { set_error("bad dw_r_block"); delete p; return SYMCON_EINVAL; }
   p->source = generate_source(p->t, p->kc);
   *out = p;
   return SYMCON_OK;
@@ -361,6 +425,38 @@ symcon_status symcon_build_tables(int lmax_in, int correlation, const int* out_L
     if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_bwd2_dW, p->lib, "symcon_bwd2_dW"), "get symcon_bwd2_dW");
     if (!s && (p->kc.gamma & 1)) s = cuda_err(cudaLibraryGetKernel(&p->k_fwd_g, p->lib, "symcon_fwd_g"), "get symcon_fwd_g");
     if (!s && (p->kc.gamma & 2)) s = cuda_err(cudaLibraryGetKernel(&p->k_dA_g, p->lib, "symcon_bwd_dA_g"), "get symcon_bwd_dA_g");
+    if (!s && p->kc.fwd_r) {
+      s = cuda_err(cudaLibraryGetKernel(&p->k_fwd_r, p->lib, "symcon_fwd_r"), "get symcon_fwd_r");
+      p->fwd_r_smem = sizeof(float) * 2 * (size_t)p->kc.fwd_r_block * 512 + 16 + sizeof(int) * 2 * (size_t)p->kc.fwd_r_block;
+      if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_fwd_r, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                           (int)p->fwd_r_smem, device), "fwd_r smem attribute");
+      int sms = 0, occ = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+      if (!s) s = cuda_err(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)p->k_fwd_r, 32 * p->t.out_per_ch,
+                                                                         p->fwd_r_smem), "occupancy fwd_r");
+      if (p->kc.fwd_r_ctas_per_sm > 0) occ = std::min(occ, p->kc.fwd_r_ctas_per_sm);
+      p->grid_fwd_r = sms * std::max(occ, 1);
+    }
+    if (!s && p->kc.da_s) {
+      s = cuda_err(cudaLibraryGetKernel(&p->k_dA_s, p->lib, "symcon_bwd_dA_s"), "get symcon_bwd_dA_s");
+      p->da_s_smem = sizeof(float) * (size_t)p->kc.da_s_warps * 2 * p->npad;
+      if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_dA_s, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                           (int)p->da_s_smem, device), "dA_s smem attribute");
+      int sms = 0, occ = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+      if (!s) s = cuda_err(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)p->k_dA_s, 32 * p->kc.da_s_warps,
+                                                                         p->da_s_smem), "occupancy dA_s");
+      p->grid_dA_s = sms * std::max(occ, 1);
+    }
+    if (!s && p->kc.dw_r && p->t.K % 32 == 0) {
+      s = cuda_err(cudaLibraryGetKernel(&p->k_dW_r, p->lib, "symcon_bwd_dW_r"), "get symcon_bwd_dW_r");
+      size_t dbw = 0;
+      for (int L : p->t.out_L) dbw += 32 * (2 * L + 1);
+      p->dw_r_smem = sizeof(float) * 2 * (size_t)p->kc.dw_r_block * (512 + dbw) + 16 + sizeof(int) * (2 * (size_t)p->kc.dw_r_block + 1);
+      if (p->kc.dw_r_fuse) p->dw_r_smem = std::max(p->dw_r_smem, sizeof(float) * (size_t)p->npad * 33);   // the S table aliases the ring
+      if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_dW_r, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                           (int)p->dw_r_smem, device), "dW_r smem attribute");
+    }
     p->tile_smem = sizeof(float) * (size_t)p->kc.tile_warps * (2 * (size_t)p->npad) + 16 * (size_t)p->kc.tile_warps;
     if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                          (int)p->tile_smem, device), "fwd smem attribute");
@@ -522,6 +618,9 @@ static void fill_params(const symcon_plan* p, const WsLayout& w, char* ws, int64
   q.spart = (float*)(ws + w.spart);
   q.tile_perm = (const int*)(ws + w.tile_perm);
   q.stot = (float*)(ws + w.stot);
+  q.coef_r = (float*)(ws + w.coef_r);
+  q.dw_count = (int*)(ws + w.dw_count);
+  q.accum = 0;
   q.N = (int)N;
   q.K = p->t.K;
   q.E = p->t.E;
@@ -563,6 +662,8 @@ static int launch_prep(const symcon_plan* p, const WsLayout& w, char* ws, int64_
   b.tile_perm = (int*)(ws + w.tile_perm);
   b.max_tiles = w.max_tiles;
   b.chunk_bad = (int*)(ws + w.chunk_bad);
+  b.zero_buf = (int*)(ws + w.dw_count);
+  b.zero_n = p->t.E * ((p->t.K + 31) / 32);
   {
     Timed tm(p, K_BUCKET, st);
     n += bucket_launch(b, st);
@@ -596,10 +697,14 @@ symcon_status symcon_forward(const symcon_plan* p, int64_t N, const float* A, co
   q.B = B;
   int n = launch_prep(p, w, (char*)ws, N, ne, W, q, st, true, &s);
   if (s) return s;
+  if (p->k_fwd_r && (s = encode_a_map(q.tmA, A, N, p->t.K, p->t.n_lm))) return s;
   void* args[] = {&q};
   {
     Timed tm(p, K_FWD, st);
-    if (p->k_fwd_g)
+    if (p->k_fwd_r)
+      s = cuda_err(cudaLaunchKernel((const void*)p->k_fwd_r, dim3(p->grid_fwd_r), dim3(32 * p->t.out_per_ch), args, p->fwd_r_smem, st),
+                   "launch symcon_fwd_r");
+    else if (p->k_fwd_g)
       s = cuda_err(cudaLaunchKernel((const void*)p->k_fwd_g, dim3((unsigned)((w.max_tiles + 3) / 4), (p->t.K + 31) / 32), dim3(128),
                                     args, 0, st), "launch symcon_fwd_g");
     else
@@ -644,26 +749,38 @@ symcon_status symcon_backward_ex(const symcon_plan* p, int64_t N, const float* A
   q.dW = dW;
   int n = launch_prep(p, w, (char*)ws, N, ne, W, q, st, dA != nullptr, &s, flags);
   if (s) return s;
+  if (dW && p->k_dW_r && (s = encode_a_map(q.tmA, A, N, p->t.K, p->t.n_lm))) return s;
   void* args[] = {&q};
   const unsigned ky = (p->t.K + p->kc.warps_per_cta - 1) / p->kc.warps_per_cta;
   if (dW) {
     {
     Timed tm(p, K_DW, st);
-    s = cuda_err(cudaLaunchKernel((const void*)p->k_dW, dim3((unsigned)(w.max_items * p->dw_nz), (p->t.K + 31) / 32, 1),
-                                  dim3(32 * p->dw_gpc), args, p->dw_smem, st), "launch symcon_bwd_dW");
+    if (p->k_dW_r)   // S partials (+ with dw_r_fuse the element's item reduction and the unfold)
+      s = cuda_err(cudaLaunchKernel((const void*)p->k_dW_r, dim3((unsigned)(w.max_items + (p->kc.dw_r_fuse ? p->t.E : 0)), p->t.K / 32, 1),
+                                    dim3(32 * p->t.out_per_ch), args, p->dw_r_smem, st), "launch symcon_bwd_dW_r");
+    else
+      s = cuda_err(cudaLaunchKernel((const void*)p->k_dW, dim3((unsigned)(w.max_items * p->dw_nz), (p->t.K + 31) / 32, 1),
+                                    dim3(32 * p->dw_gpc), args, p->dw_smem, st), "launch symcon_bwd_dW");
     }
     if (s) return s;
-    Timed tm(p, K_UNFOLD, st);
-    n += reduce_items_launch(q.spart, q.item_off, p->t.E, p->npad, p->t.K, q.stot, st);
-    s = cuda_err(cudaLaunchKernel((const void*)p->k_unfold, dim3(p->t.E, (p->t.K + 31) / 32), dim3(512), args,
-                                  p->unfold_smem, st), "launch symcon_unfold");
-    if (s) return s;
-    n += 2;
+    if (!p->k_dW_r || !p->kc.dw_r_fuse) {
+      Timed tm(p, K_UNFOLD, st);
+      n += reduce_items_launch(q.spart, q.item_off, p->t.E, p->npad, p->t.K, q.stot, st);
+      s = cuda_err(cudaLaunchKernel((const void*)p->k_unfold, dim3(p->t.E, (p->t.K + 31) / 32), dim3(512), args,
+                                    p->unfold_smem, st), "launch symcon_unfold");
+      if (s) return s;
+      n += 2;
+    } else {
+      n += 1;
+    }
   }
   if (dA) {
     {
     Timed tm(p, K_DA, st);
-    if (p->k_dA_g)
+    if (p->k_dA_s)
+      s = cuda_err(cudaLaunchKernel((const void*)p->k_dA_s, dim3(p->grid_dA_s), dim3(32 * p->kc.da_s_warps), args, p->da_s_smem, st),
+                   "launch symcon_bwd_dA_s");
+    else if (p->k_dA_g)
       s = cuda_err(cudaLaunchKernel((const void*)p->k_dA_g, dim3((unsigned)((w.max_tiles + 3) / 4), (p->t.K + 31) / 32), dim3(128),
                                     args, 0, st), "launch symcon_bwd_dA_g");
     else

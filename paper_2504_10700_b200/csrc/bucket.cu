@@ -45,13 +45,16 @@ __global__ void __launch_bounds__(1024) bk_scan(const int* __restrict__ hist, in
                         int* __restrict__ seg_off, int4* __restrict__ tiles, int* __restrict__ n_tiles,
                         int4* __restrict__ items, int* __restrict__ n_items, int* __restrict__ item_off,
                         int* __restrict__ tile_off, int* __restrict__ tile_perm, int tile_nodes, int tiles_per_item,
-                        const int* __restrict__ chunk_bad, unsigned long long* __restrict__ err) {
+                        const int* __restrict__ chunk_bad, unsigned long long* __restrict__ err,
+                        int* __restrict__ zero_buf, int zero_n) {
   extern __shared__ int sm[];   // tot[E+1], tile_off[E+1], itm_off[E+1]
   int* tot = sm;
   int* toff = sm + (E + 1);
   int* ioff = sm + 2 * (E + 1);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5, E1 = E + 1;
   for (int e = tid; e <= E; e += blockDim.x) tot[e] = 0;
+  if (zero_buf)
+    for (int x = tid; x < zero_n; x += blockDim.x) zero_buf[x] = 0;
   __syncthreads();
   // 1. element totals: coalesced pass over the [chunk][E+1] histogram with smem atomics
   for (int x = tid; x < nchunks * E1; x += blockDim.x) {
@@ -263,7 +266,7 @@ int bucket_launch(const BucketArgs& a, cudaStream_t st) {
   if (3 * sm_e > 48 * 1024) cudaFuncSetAttribute(bk_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * sm_e));
   bk_scan<<<1, 1024, 3 * sm_e, st>>>(a.hist, nchunks, a.E, a.off, a.seg_off, a.tiles, a.n_tiles, a.items,
                                     a.n_items, a.item_off, a.tile_off, a.tile_perm, a.tile_nodes, a.tiles_per_item,
-                                    a.chunk_bad, a.err);
+                                    a.chunk_bad, a.err, a.zero_buf, a.zero_n);
   if (a.N > 0) {
     if (a.E + 1 <= kWarpE && 32 * sm_e > 48 * 1024)
       cudaFuncSetAttribute(bk_scatter_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(32 * sm_e));

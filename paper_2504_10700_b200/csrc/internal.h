@@ -78,8 +78,30 @@ struct KernelConfig {
   int dw_batch = 1;                // transposed dW: rows whose products are emitted before their FMAs
   int dw_block_nodes = 8;          // transposed dW: nodes per smem stage
   int unfold_channels = 8;   // channels per unfold CTA
+  int fwd_r = -1;            // forward as symcon_fwd_r (lane = channel, warp = output slot, Horner); -1 auto
+  int fwd_r_block = 16;       // fwd_r: nodes per shared-memory block (even, divides 64)
+  int fwd_r_minb = 3;        // fwd_r: __launch_bounds__ min blocks (0 = none; 3 caps MP-medium at 170 registers)
+  int fwd_r_ctas_per_sm = 0; // fwd_r: persistent CTAs per SM (0 = occupancy maximum)
+  int dw_r = -1;             // dW as symcon_bwd_dW_r (lane = channel, warp = output slot, q-form); -1 auto
+  int dw_r_block = 8;        // dw_r: nodes per shared-memory block
+  int dw_r_minb = 0;         // dw_r: __launch_bounds__ min blocks
+  int dw_r_unroll = 1;       // dw_r: node-loop unroll
+  int dw_r_fuse = 0;         // dw_r: the last CTA of each (element, channel block) reduces + unfolds in-kernel
+  int da_s = -1;             // dA as symcon_bwd_dA_s (one node per lane, scalar FP32); -1 auto
+  int da_s_warps = 4;        // da_s: warps (channels) per CTA
+  int da_s_minb = 0;         // da_s: __launch_bounds__ min blocks
 };
 std::string generate_source(const Tables& t, const KernelConfig& kc);
+
+// Horner program of one output slot (symcon_fwd_r)
+struct HornerB { int b, row_ab; std::vector<std::pair<int, int>> cs; };   // (c, row j) of degree-3 rows
+struct HornerA { int a, row_a; std::vector<HornerB> bs; };
+struct HornerSlot { int slot; std::vector<HornerA> as; std::vector<int> rows; };  // rows: register order
+std::vector<HornerSlot> horner_slots(const Tables& t);
+int64_t horner_ops(const Tables& t);
+std::string generate_fwd_r(const Tables& t, const KernelConfig& kc);
+std::string generate_dw_r(const Tables& t, const KernelConfig& kc);
+std::string generate_da_s(const Tables& t, const KernelConfig& kc);
 // apply "key=value,..." overrides (env SYMCON_KCONFIG) to a KernelConfig; returns false on bad keys
 bool parse_kernel_config(const char* spec, KernelConfig& kc);
 

@@ -22,6 +22,8 @@ struct BucketArgs {
   int64_t max_tiles;
   int* chunk_bad;  // [nchunks] first out-of-range node of each chunk
   unsigned long long* err;
+  int* zero_buf;   // zeroed by bk_scan (dW_r per-(element, channel block) item counters), may be NULL
+  int zero_n;
 };
 
 int bucket_launch(const BucketArgs& a, cudaStream_t st);   // returns launches issued

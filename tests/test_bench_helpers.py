@@ -24,8 +24,9 @@ def test_alg_ops_matches_design_counts(L):
     sc = S()
     sc.plan = L.symcon_build_tables(3, 3, [0, 1], 89, 128, -1)
     ops = bench.alg_ops(sc)
-    # DESIGN.md §7 table (MP-medium)
-    assert (ops["fwd"], ops["dA"], ops["dW"], ops["path"], ops["bwd2"], ops["bwd2_dW"]) == (888, 1486, 888, 3146, 3431, 1482)
+    # DESIGN.md §7 table (MP-medium): Horner forward 705, reverse-Horner dW 731
+    assert (ops["fwd"], ops["dA"], ops["dW"], ops["path"], ops["bwd2"], ops["bwd2_dW"]) == (705, 1486, 731, 2922, 3431, 1482)
+    assert (ops["fwd_monomial_first"], ops["dW_monomial_first"], ops["path_monomial_first"]) == (888, 888, 3146)
     assert ops["n_fold"] == 410 and ops["prefixes"] == 123 and ops["deg3_monomials"] == 355
     L.symcon_destroy(sc.plan)
 
