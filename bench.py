@@ -34,6 +34,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CAPACITY = 50_000
+# BASELINE.json configs: MP-medium = a 50k-node batch, large = a 200k-node batch (both Alg. 1 bins of the
+# Table-2 manifest), OFF-small = a 20k-node batch of 10-100-atom molecules (organic element mix)
+DEFAULT_CAPACITY = {"mp_medium": 50_000, "large": 200_000, "off_small": None}
+OFF_BATCH_NODES = 20_000
 POOL = 4
 EDGE_DEGREE = 30   # synthetic in-degree min(30, n-1)
 
@@ -45,8 +49,9 @@ def parse(argv=None):
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="mp_medium", choices=["off_small", "mp_medium", "large"])
-    ap.add_argument("--capacity", type=int, default=CAPACITY,
-                    help="Alg. 1 bin capacity in nodes per GPU-step (paper: 3072, PAPER.md:969)")
+    ap.add_argument("--capacity", type=int, default=None,
+                    help="Alg. 1 bin capacity in nodes per GPU-step (default: 50,000 mp_medium, 200,000 large; "
+                         "the paper's 3072, PAPER.md:969); off_small uses 20k-node molecule batches instead")
     ap.add_argument("--cpu-sample", type=int, default=32768, help="nodes in the oracle's bounded sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-overlap", action="store_true", help="all-reduce dW after dA instead of overlapping")
@@ -67,7 +72,10 @@ def parse(argv=None):
     ap.add_argument("--double-backward", action="store_true",
                     help="force-training step (SURVEY §8(f) row 1): fwd + bwd + the double backward "
                          "(dB_bar, A_bar, W_bar of <uA, dA>) per step; metric symcon_fwd_bwd_bwd2_nodes_per_s")
-    return ap.parse_args(argv)
+    a = ap.parse_args(argv)
+    if a.capacity is None:
+        a.capacity = DEFAULT_CAPACITY[a.config]
+    return a
 
 
 # ----------------------------------------------------------------------------- workload
@@ -116,6 +124,19 @@ def bin_inputs(cfg, sizes, offs, ids, b, q, rank, out_dim, n_lm, device):
     A = gen_A(N, cfg.channels, n_lm, device, seed=100 * q + rank)
     dB = gen_dB(N, out_dim, device, seed=100 * q + rank)
     return ne, A, dB
+
+
+def molecule_batch(cfg, q, rank, out_dim, n_lm, device):
+    """OFF-small (BASELINE.json configs[1]): a 20k-node batch of U[10, 100]-atom molecules with the organic
+    element mix per node; pool entry q of `rank`. Returns (sizes, node_elem, A, dB)."""
+    import torch
+    from synth.inputs import gen_A, gen_dB, gen_node_elem, molecule_sizes
+    sizes = np.array(molecule_sizes(OFF_BATCH_NODES, 10, 100, seed=100 * q + rank), dtype=np.int64)
+    N = int(sizes.sum())
+    ne = gen_node_elem(N, cfg.n_elements, cfg.elem_dist, device, seed=100 * q + rank)
+    A = gen_A(N, cfg.channels, n_lm, device, seed=100 * q + rank)
+    dB = gen_dB(N, out_dim, device, seed=100 * q + rank)
+    return sizes, ne, A, dB
 
 
 def edge_spread(sizes, offs, ids, world, steps):
@@ -347,11 +368,14 @@ def run_reference(args):
     oc = OracleC(prob)
     world = max(args.gpus, 1)
     t0 = time.time()
-    sizes, offs, ids = plan_bins_oracle(world, args.capacity)
-    t_pack = time.time() - t0
-    b = 0   # pool entry 0 of rank 0 = step 0's bin of rank 0
     n_lm = (cfg.lmax_in + 1) ** 2
-    ne_t, A_t, dB_t = bin_inputs(cfg, sizes, offs, ids, b, 0, 0, prob.out_dim(cfg.channels), n_lm, "cpu")
+    if args.capacity is None:   # off_small: the GPU arm's first molecule batch of rank 0
+        _, ne_t, A_t, dB_t = molecule_batch(cfg, 0, 0, prob.out_dim(cfg.channels), n_lm, "cpu")
+    else:
+        sizes, offs, ids = plan_bins_oracle(world, args.capacity)
+        b = 0   # pool entry 0 of rank 0 = step 0's bin of rank 0
+        ne_t, A_t, dB_t = bin_inputs(cfg, sizes, offs, ids, b, 0, 0, prob.out_dim(cfg.channels), n_lm, "cpu")
+    t_pack = time.time() - t0
     ne_full, A_full, dB_full = ne_t.numpy(), A_t.numpy(), dB_t.numpy()
     n_bin = len(ne_full)
     W = gen_W(cfg.n_elements, prob.block_sizes(), cfg.channels, "cpu").numpy()
@@ -377,8 +401,8 @@ def run_reference(args):
            "config": workload_config(args, cfg, n_bin),
            "same_config": True,
            "cpu_baseline": {"value": v, "unit": "nodes/s", "cores": oc.threads(), "kind": "oracle",
-                            "sample": f"{per_step} nodes per step (seeded permutation of bin 0, the GPU arm's pool entry 0 "
-                                      f"on rank 0: same Alg. 1 bin, node elements, A, dB, W) x {args.steps} steps"},
+                            "sample": f"{per_step} nodes per step (seeded permutation of batch 0, the GPU arm's pool entry 0 "
+                                      f"on rank 0: same batch, node elements, A, dB, W) x {args.steps} steps"},
            "alg1_pack_s": round(t_pack, 3), "oracle_only": "oracle/packing.py + oracle/csrc/oracle_eval.c; libsymcon not loaded",
            "e2e": {"value": v, "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -386,7 +410,9 @@ def run_reference(args):
 
 def workload_config(args, cfg, nodes_per_bin):
     return {"workload": f"{args.config}_dp_step" + ("_double_backward" if args.double_backward else "")
-                        + ("" if args.capacity == CAPACITY else f"_C{args.capacity}"),
+                        + ("" if args.capacity == DEFAULT_CAPACITY[args.config] else f"_C{args.capacity}"),
+            "batch": ("20k-node batches of U[10,100]-atom molecules, organic element mix" if args.capacity is None else
+                      f"Alg. 1 bins of the Table-2 manifest, capacity {args.capacity} nodes"),
             "model": "MACE symmetric contraction", "channels": cfg.channels,
             "out": "+".join(f"{cfg.channels}x{L}{'e' if L % 2 == 0 else 'o'}" for L in cfg.out_L),
             "lmax_in": cfg.lmax_in, "correlation": cfg.correlation, "elements": cfg.n_elements,
@@ -414,22 +440,32 @@ class TimedStep:
         self.world, self.rank, self.double_backward = world, rank, double_backward
         self.sc = sc = SymmetricContraction(cfg.lmax_in, cfg.correlation, cfg.out_L, cfg.n_elements, cfg.channels,
                                             device=device)
-        self.sizes = table2_sizes(seed=0)
+        self.capacity = capacity
+        self.pool, self.uA, self.mol_sizes = [], {}, []
         t0 = time.time()
-        self.shards = BinPackedShards(self.sizes, capacity, world, rank)
+        if capacity is not None:
+            self.sizes = table2_sizes(seed=0)
+            self.shards = BinPackedShards(self.sizes, capacity, world, rank)
+        else:
+            self.sizes = self.shards = None
         self.t_pack = time.time() - t0
-        self.pool, self.uA = [], {}
         for q in range(pool):
-            b = self.shards.bin_of(q % self.shards.n_steps)
-            ne, A, dB = bin_inputs(cfg, self.sizes, self.shards.offsets, self.shards.ids, b, q, rank, sc.out_dim,
-                                   sc.n_lm, dev)
+            if capacity is not None:
+                b = self.shards.bin_of(q % self.shards.n_steps)
+                ne, A, dB = bin_inputs(cfg, self.sizes, self.shards.offsets, self.shards.ids, b, q, rank, sc.out_dim,
+                                       sc.n_lm, dev)
+            else:
+                b = q
+                msz, ne, A, dB = molecule_batch(cfg, q, rank, sc.out_dim, sc.n_lm, dev)
+                self.mol_sizes.append(msz)
             N = ne.numel()
             B = torch.empty((N, sc.out_dim), device=dev)
             dA = torch.empty_like(A)
             self.pool.append((b, N, A, ne, dB, B, dA))
             if double_backward:
                 self.uA[q] = gen_A(N, cfg.channels, sc.n_lm, dev, seed=100 * q + rank + 7)
-        self.imbalance = max(self.shards.step_imbalance(q % self.shards.n_steps) for q in range(pool))
+        self.imbalance = (max(self.shards.step_imbalance(q % self.shards.n_steps) for q in range(pool))
+                          if self.shards is not None else 1.0)
         self.W = gen_W(cfg.n_elements, sc.block_sizes(), cfg.channels, dev)
         if world > 1:
             import torch.distributed as dist
@@ -641,7 +677,7 @@ def run_ours(args):
         ms_step = ms_max / args.steps
         ksum = sum(v["avg_ms"] * v["launches"] for v in kernels.values()) / args.steps
         config = workload_config(args, cfg, pool[0][1])
-        config.update({"bins": ts.shards.n_bins, "global_batch": int(nodes_all / args.steps),
+        config.update({"bins": ts.shards.n_bins if ts.shards is not None else None, "global_batch": int(nodes_all / args.steps),
                        "step_imbalance_max_over_mean": round(ts.imbalance, 5),
                        "dW_allreduce": ({"peer": f"libsymcon NVLink peer-memory kernel (algo {dp._peer.algo if dp._peer else args.peer_algo}: "
                                                  "0 auto, 1 one-shot, 2 two-shot), dA concurrent",
@@ -659,7 +695,8 @@ def run_ours(args):
             "config": config,
             "per_gpu_nodes_per_s": value / world,
             "per_rank_ms_per_step": per_rank_ms,
-            "edge_balance": edge_spread(ts.sizes, ts.shards.offsets, ts.shards.ids, world, POOL),
+            "edge_balance": (edge_spread(ts.sizes, ts.shards.offsets, ts.shards.ids, world, POOL) if ts.shards is not None
+                             else {"note": "one molecule batch per rank (no Alg. 1 bins)"}),
             "path_tops": path_ops / (ms_step / 1e3) / 1e12,
             "path_frac_of_alu_peak": path_ops / (ms_step / 1e3) / 1e12 / peak_alu,
             "path_roofline": path_roofline(cfg, sc, mean_nodes, path_ops, ms_step, args.double_backward, sm_mhz),
@@ -705,7 +742,7 @@ def kernel_roofline(args, cfg, sc, ops, prof, mean_nodes, peak_alu, sm_mhz):
              "symcon_bwd2_dW": 4 * (2 * nlm + outc)}[kern] * mean_nodes * K
     traffic, tsrc = None, None
     for tpath in (os.path.join(ROOT, "profiles", "r02", "ncu_traffic.json"),):
-        if os.path.exists(tpath) and args.config == "mp_medium" and args.capacity == CAPACITY:
+        if os.path.exists(tpath) and args.config == "mp_medium" and args.capacity == DEFAULT_CAPACITY["mp_medium"]:
             tj = json.load(open(tpath))
             rec = tj["kernels"].get(kern)
             if rec:

@@ -141,6 +141,14 @@ symcon_status symcon_backward2(const symcon_plan* plan, int64_t num_nodes, const
                                const float* W, const int32_t* node_elem, const float* dB,
                                const float* uA, float* dB_bar, float* A_bar, float* W_bar, void* ws,
                                size_t ws_bytes, uint32_t flags, void* stream /* cudaStream_t */);
+/* The full double backward of (A, W, dB) -> (dA, dW) with cotangents (uA, uW): the uA terms as in
+ * symcon_backward2 plus the uW terms, computed in libsymcon (no caller arithmetic):
+ *   dB_bar += forward(A, uW)   and   A_bar += dA(A, uW, dB)   (W_bar gets no uW term: dW is linear in dB
+ *   and independent of W). uA or uW may be NULL (not both); the outputs are overwritten. */
+symcon_status symcon_backward2_ex(const symcon_plan* plan, int64_t num_nodes, const float* A,
+                                  const float* W, const int32_t* node_elem, const float* dB,
+                                  const float* uA, const float* uW, float* dB_bar, float* A_bar, float* W_bar,
+                                  void* ws, size_t ws_bytes, uint32_t flags, void* stream /* cudaStream_t */);
 
 /* Synchronises `stream`; returns SYMCON_EELEMENT and *first_bad_node if the last forward /
  * backward that used `ws` saw an out-of-range node_elem, SYMCON_ECUDA on a CUDA error. */
@@ -264,6 +272,19 @@ symcon_status symcon_tp_backward(const symcon_tp_plan* plan, int64_t num_nodes, 
                                  const float* Y, const float* h, const float* R, const int32_t* sender,
                                  const int32_t* receiver, const float* dA, float* dY, float* dh, float* dR,
                                  void* ws, size_t ws_bytes, void* stream /* cudaStream_t */);
+/* Double backward of the TP (the derivatives of <(uY, uh, uR), (dY, dh, dR)(Y, h, R, dA)> and of <uA_bar...>:
+ * the TP is linear in each of Y, h, R, so every term is a TP pass with one input replaced by its
+ * cotangent, summed on the device (no caller arithmetic):
+ *   dA_bar = TP(uY,h,R) + TP(Y,uh,R) + TP(Y,h,uR)
+ *   Y_bar  = dY|(h:=uh) + dY|(R:=uR),  h_bar = dh|(R:=uR) + dh|(Y:=uY),  R_bar = dR|(h:=uh) + dR|(Y:=uY)
+ * Outputs overwritten, any may be NULL. ws needs symcon_tp_workspace2_bytes (the TP workspace plus
+ * one temporary of each output's size). */
+size_t symcon_tp_workspace2_bytes(const symcon_tp_plan* plan, int64_t num_nodes, int64_t num_edges);
+symcon_status symcon_tp_backward2(const symcon_tp_plan* plan, int64_t num_nodes, int64_t num_edges,
+                                  const float* Y, const float* h, const float* R, const int32_t* sender,
+                                  const int32_t* receiver, const float* dA, const float* uY, const float* uh,
+                                  const float* uR, float* dA_bar, float* Y_bar, float* h_bar, float* R_bar,
+                                  void* ws, size_t ws_bytes, void* stream /* cudaStream_t */);
 /* Synchronises `stream`; SYMCON_EINVAL if the last TP call on `ws` saw unsorted receivers or an
  * out-of-range node index (*first_bad_edge = the first such edge), SYMCON_ECUDA on CUDA errors. */
 symcon_status symcon_tp_check_device_error(const symcon_tp_plan* plan, void* ws, void* stream,

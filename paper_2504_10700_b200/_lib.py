@@ -27,7 +27,7 @@ EXPORTS = ["symcon_build_tables", "symcon_plan_info", "symcon_plan_path", "symco
            "symcon_tp_workspace_bytes", "symcon_tp_forward", "symcon_tp_backward", "symcon_tp_check_device_error",
            "symcon_tp_last_launch_count", "symcon_tp_source", "symcon_tp_destroy", "symcon_peer_allreduce",
            "symcon_tp_precompile", "symcon_peer_allreduce_dev", "symcon_peer_allreduce_ex", "symcon_peer_check",
-           "symcon_peer_allreduce_emulate"]
+           "symcon_peer_allreduce_emulate", "symcon_backward2_ex", "symcon_tp_backward2", "symcon_tp_workspace2_bytes"]
 
 
 class SymconInfo(ctypes.Structure):
@@ -52,6 +52,8 @@ lib.symcon_forward.argtypes = [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
 lib.symcon_backward.argtypes = [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
 lib.symcon_backward_ex.argtypes = [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, ctypes.c_uint32, _vp]
 lib.symcon_backward2.argtypes = [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, ctypes.c_uint32, _vp]
+lib.symcon_backward2_ex.argtypes = [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, ctypes.c_uint32, _vp]
+lib.symcon_backward2_ex.restype = ctypes.c_int
 SYMCON_REUSE_BUCKETS, SYMCON_REUSE_FOLD = 1, 2
 lib.symcon_check_device_error.argtypes = [_vp, _vp, _vp, ctypes.POINTER(_i64)]
 lib.symcon_last_launch_count.argtypes = [_vp]
@@ -164,6 +166,11 @@ def symcon_backward2(plan, num_nodes, A, W, node_elem, dB, uA, dB_bar, A_bar, W_
           "symcon_backward2")
 
 
+def symcon_backward2_ex(plan, num_nodes, A, W, node_elem, dB, uA, uW, dB_bar, A_bar, W_bar, ws, ws_bytes, flags, stream):
+    check(lib.symcon_backward2_ex(plan, num_nodes, A, W, node_elem, dB, uA, uW, dB_bar, A_bar, W_bar, ws, ws_bytes, flags,
+                                  stream), "symcon_backward2_ex")
+
+
 def symcon_check_device_error(plan, ws, stream):
     bad = _i64(-1)
     s = lib.symcon_check_device_error(plan, ws, stream, ctypes.byref(bad))
@@ -261,6 +268,22 @@ def symcon_tp_path(plan, p):
 
 def symcon_tp_workspace_bytes(plan, num_nodes, num_edges):
     return lib.symcon_tp_workspace_bytes(plan, num_nodes, num_edges)
+
+
+lib.symcon_tp_workspace2_bytes.argtypes = [_vp, _i64, _i64]
+lib.symcon_tp_workspace2_bytes.restype = _sz
+lib.symcon_tp_backward2.argtypes = [_vp, _i64, _i64] + [_vp] * 14 + [_sz, _vp]
+lib.symcon_tp_backward2.restype = ctypes.c_int
+
+
+def symcon_tp_workspace2_bytes(plan, num_nodes, num_edges):
+    return lib.symcon_tp_workspace2_bytes(plan, num_nodes, num_edges)
+
+
+def symcon_tp_backward2(plan, N, E, Y, h, R, sender, receiver, dA, uY, uh, uR, dA_bar, Y_bar, h_bar, R_bar, ws, ws_bytes,
+                        stream):
+    check(lib.symcon_tp_backward2(plan, N, E, Y, h, R, sender, receiver, dA, uY, uh, uR, dA_bar, Y_bar, h_bar, R_bar, ws,
+                                  ws_bytes, stream), "symcon_tp_backward2")
 
 
 def symcon_tp_forward(plan, N, E, Y, h, R, sender, receiver, A, ws, ws_bytes, stream):

@@ -158,7 +158,7 @@ symcon_status encode_a_map(TmapA& m, const float* A, int64_t N, int K, int n_lm)
 
 struct WsLayout {
   size_t hist, chunk_bad, off, seg_off, perm, tiles, n_tiles, items, n_items, item_off, err, coef, spart, tile_off, tile_perm, stot,
-      coef_r, dw_count, total;
+      coef_r, dw_count, coef2, coef_r2, total;
   int64_t max_tiles, max_items;
 };
 
@@ -190,6 +190,8 @@ WsLayout layout(const symcon_plan* p, int64_t N) {
   w.stot = take(sizeof(float) * (size_t)E * K * p->npad);
   w.coef_r = take(sizeof(float) * (size_t)E * p->t.out_per_ch * std::max(p->rnq, 1) * K * 4);
   w.dw_count = take(sizeof(int) * (size_t)E * ((K + 31) / 32));
+  w.coef2 = take(sizeof(float) * (size_t)E * K * p->npad);   // the uW fold of the double backward
+  w.coef_r2 = take(sizeof(float) * (size_t)E * p->t.out_per_ch * std::max(p->rnq, 1) * K * 4);
   w.total = o;
   return w;
 }
@@ -368,6 +370,9 @@ static symcon_status build_common(int lmax_in, int corr, const int* out_L, int n
   // measured (profiles/r02): fwd_r beats symcon_fwd at 1 and 4 output slots (OFF-small, MP-medium) and
   // loses at 9 (large: 9 warps x 166 registers per CTA)
   if (p->kc.fwd_r < 0) p->kc.fwd_r = p->t.out_per_ch <= 4 ? 1 : 0;
+  if (p->kc.fold_split < 1 || p->kc.fold_split > 16) { set_error("bad fold_split"); delete p; return SYMCON_EINVAL; }
+  if (p->kc.fwd_r_nst < 2 || p->kc.fwd_r_nst > 8 || p->kc.dw_r_nst < 2 || p->kc.dw_r_nst > 8) { set_error("bad ring depth"); delete p; return SYMCON_EINVAL; }
+  if (p->kc.fwd_r_tr) { set_error("fwd_r_tr is not available with the mbarrier ring"); delete p; return SYMCON_EINVAL; }
   if (p->kc.fwd_r_block < 2 || p->kc.fwd_r_block > 32 || (p->kc.fwd_r_block & 1) || 64 % p->kc.fwd_r_block) {
     set_error("bad fwd_r_block");
     delete p;
@@ -427,7 +432,9 @@ symcon_status symcon_build_tables(int lmax_in, int correlation, const int* out_L
     if (!s && (p->kc.gamma & 2)) s = cuda_err(cudaLibraryGetKernel(&p->k_dA_g, p->lib, "symcon_bwd_dA_g"), "get symcon_bwd_dA_g");
     if (!s && p->kc.fwd_r) {
       s = cuda_err(cudaLibraryGetKernel(&p->k_fwd_r, p->lib, "symcon_fwd_r"), "get symcon_fwd_r");
-      p->fwd_r_smem = sizeof(float) * 2 * (size_t)p->kc.fwd_r_block * 512 + 16 + sizeof(int) * 2 * (size_t)p->kc.fwd_r_block;
+      p->fwd_r_smem = sizeof(float) * p->kc.fwd_r_nst * (size_t)p->kc.fwd_r_block * 512 + 16 * p->kc.fwd_r_nst +
+                      sizeof(int) * p->kc.fwd_r_nst * (size_t)p->kc.fwd_r_block;
+      if (p->kc.fwd_r_tr) p->fwd_r_smem += sizeof(float) * (size_t)p->kc.fwd_r_block * 512 + 64;   // the interleaved copy
       if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_fwd_r, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                            (int)p->fwd_r_smem, device), "fwd_r smem attribute");
       int sms = 0, occ = 0;
@@ -452,7 +459,8 @@ symcon_status symcon_build_tables(int lmax_in, int correlation, const int* out_L
       s = cuda_err(cudaLibraryGetKernel(&p->k_dW_r, p->lib, "symcon_bwd_dW_r"), "get symcon_bwd_dW_r");
       size_t dbw = 0;
       for (int L : p->t.out_L) dbw += 32 * (2 * L + 1);
-      p->dw_r_smem = sizeof(float) * 2 * (size_t)p->kc.dw_r_block * (512 + dbw) + 16 + sizeof(int) * (2 * (size_t)p->kc.dw_r_block + 1);
+      p->dw_r_smem = sizeof(float) * p->kc.dw_r_nst * (size_t)p->kc.dw_r_block * (512 + dbw) + 16 * p->kc.dw_r_nst +
+                     sizeof(int) * (p->kc.dw_r_nst * (size_t)p->kc.dw_r_block + 1);
       if (p->kc.dw_r_fuse) p->dw_r_smem = std::max(p->dw_r_smem, sizeof(float) * (size_t)p->npad * 33);   // the S table aliases the ring
       if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_dW_r, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                            (int)p->dw_r_smem, device), "dW_r smem attribute");
@@ -664,6 +672,7 @@ static int launch_prep(const symcon_plan* p, const WsLayout& w, char* ws, int64_
   b.chunk_bad = (int*)(ws + w.chunk_bad);
   b.zero_buf = (int*)(ws + w.dw_count);
   b.zero_n = p->t.E * ((p->t.K + 31) / 32);
+  b.fused = p->kc.bucket_fused;
   {
     Timed tm(p, K_BUCKET, st);
     n += bucket_launch(b, st);
@@ -673,11 +682,41 @@ after_bucket:
     Timed tm(p, K_FOLD, st);
     q.W = W;
     void* args[] = {&q};
-    dim3 grid(p->t.E, (p->t.K + 31) / 32);
+    dim3 grid(p->t.E, (p->t.K + 31) / 32, p->kc.fold_split);
     *s = cuda_err(cudaLaunchKernel((const void*)p->k_fold, grid, dim3(128), args, 0, st), "launch symcon_fold");
     n++;
   }
   return n;
+}
+
+// the forward kernel of the plan (fwd_r / gamma / persistent) with the coefficients q.coef(_r) already folded
+static symcon_status launch_fwd_kernel(const symcon_plan* p, const WsLayout& w, Params& q, int64_t N, cudaStream_t st) {
+  symcon_status s = SYMCON_OK;
+  if (p->k_fwd_r && (s = encode_a_map(q.tmA, q.A, N, p->t.K, p->t.n_lm))) return s;
+  void* args[] = {&q};
+  Timed tm(p, K_FWD, st);
+  if (p->k_fwd_r)
+    return cuda_err(cudaLaunchKernel((const void*)p->k_fwd_r, dim3(p->grid_fwd_r), dim3(32 * p->t.out_per_ch), args, p->fwd_r_smem, st),
+                    "launch symcon_fwd_r");
+  if (p->k_fwd_g)
+    return cuda_err(cudaLaunchKernel((const void*)p->k_fwd_g, dim3((unsigned)((w.max_tiles + 3) / 4), (p->t.K + 31) / 32), dim3(128),
+                                     args, 0, st), "launch symcon_fwd_g");
+  return cuda_err(cudaLaunchKernel((const void*)p->k_fwd, dim3(p->grid_fwd), dim3(32 * p->kc.tile_warps), args, p->tile_smem, st),
+                  "launch symcon_fwd");
+}
+
+// the dA kernel of the plan (scalar / gamma / persistent)
+static symcon_status launch_dA_kernel(const symcon_plan* p, const WsLayout& w, Params& q, cudaStream_t st) {
+  void* args[] = {&q};
+  Timed tm(p, K_DA, st);
+  if (p->k_dA_s)
+    return cuda_err(cudaLaunchKernel((const void*)p->k_dA_s, dim3(p->grid_dA_s), dim3(32 * p->kc.da_s_warps), args, p->da_s_smem, st),
+                    "launch symcon_bwd_dA_s");
+  if (p->k_dA_g)
+    return cuda_err(cudaLaunchKernel((const void*)p->k_dA_g, dim3((unsigned)((w.max_tiles + 3) / 4), (p->t.K + 31) / 32), dim3(128),
+                                     args, 0, st), "launch symcon_bwd_dA_g");
+  return cuda_err(cudaLaunchKernel((const void*)p->k_dA, dim3(p->grid_dA), dim3(32 * p->kc.tile_warps), args, p->tile_smem, st),
+                  "launch symcon_bwd_dA");
 }
 
 symcon_status symcon_forward(const symcon_plan* p, int64_t N, const float* A, const float* W, const int32_t* ne,
@@ -697,20 +736,7 @@ symcon_status symcon_forward(const symcon_plan* p, int64_t N, const float* A, co
   q.B = B;
   int n = launch_prep(p, w, (char*)ws, N, ne, W, q, st, true, &s);
   if (s) return s;
-  if (p->k_fwd_r && (s = encode_a_map(q.tmA, A, N, p->t.K, p->t.n_lm))) return s;
-  void* args[] = {&q};
-  {
-    Timed tm(p, K_FWD, st);
-    if (p->k_fwd_r)
-      s = cuda_err(cudaLaunchKernel((const void*)p->k_fwd_r, dim3(p->grid_fwd_r), dim3(32 * p->t.out_per_ch), args, p->fwd_r_smem, st),
-                   "launch symcon_fwd_r");
-    else if (p->k_fwd_g)
-      s = cuda_err(cudaLaunchKernel((const void*)p->k_fwd_g, dim3((unsigned)((w.max_tiles + 3) / 4), (p->t.K + 31) / 32), dim3(128),
-                                    args, 0, st), "launch symcon_fwd_g");
-    else
-      s = cuda_err(cudaLaunchKernel((const void*)p->k_fwd, dim3(p->grid_fwd), dim3(32 * p->kc.tile_warps), args, p->tile_smem, st),
-                   "launch symcon_fwd");
-  }
+  s = launch_fwd_kernel(p, w, q, N, st);
   n++;
   if (s) return s;
   p->last_launches = n;
@@ -757,7 +783,8 @@ symcon_status symcon_backward_ex(const symcon_plan* p, int64_t N, const float* A
     Timed tm(p, K_DW, st);
     if (p->k_dW_r)   // S partials (+ with dw_r_fuse the element's item reduction and the unfold)
       s = cuda_err(cudaLaunchKernel((const void*)p->k_dW_r, dim3((unsigned)(w.max_items + (p->kc.dw_r_fuse ? p->t.E : 0)), p->t.K / 32, 1),
-                                    dim3(32 * p->t.out_per_ch), args, p->dw_r_smem, st), "launch symcon_bwd_dW_r");
+                                    dim3(32 * p->t.out_per_ch * std::max(1, p->kc.dw_r_split)), args, p->dw_r_smem, st),
+                   "launch symcon_bwd_dW_r");
     else
       s = cuda_err(cudaLaunchKernel((const void*)p->k_dW, dim3((unsigned)(w.max_items * p->dw_nz), (p->t.K + 31) / 32, 1),
                                     dim3(32 * p->dw_gpc), args, p->dw_smem, st), "launch symcon_bwd_dW");
@@ -765,7 +792,7 @@ symcon_status symcon_backward_ex(const symcon_plan* p, int64_t N, const float* A
     if (s) return s;
     if (!p->k_dW_r || !p->kc.dw_r_fuse) {
       Timed tm(p, K_UNFOLD, st);
-      n += reduce_items_launch(q.spart, q.item_off, p->t.E, p->npad, p->t.K, q.stot, st);
+      if (!p->kc.unfold_reduce) n += reduce_items_launch(q.spart, q.item_off, p->t.E, p->npad, p->t.K, q.stot, st);
       s = cuda_err(cudaLaunchKernel((const void*)p->k_unfold, dim3(p->t.E, (p->t.K + 31) / 32), dim3(512), args,
                                     p->unfold_smem, st), "launch symcon_unfold");
       if (s) return s;
@@ -775,18 +802,7 @@ symcon_status symcon_backward_ex(const symcon_plan* p, int64_t N, const float* A
     }
   }
   if (dA) {
-    {
-    Timed tm(p, K_DA, st);
-    if (p->k_dA_s)
-      s = cuda_err(cudaLaunchKernel((const void*)p->k_dA_s, dim3(p->grid_dA_s), dim3(32 * p->kc.da_s_warps), args, p->da_s_smem, st),
-                   "launch symcon_bwd_dA_s");
-    else if (p->k_dA_g)
-      s = cuda_err(cudaLaunchKernel((const void*)p->k_dA_g, dim3((unsigned)((w.max_tiles + 3) / 4), (p->t.K + 31) / 32), dim3(128),
-                                    args, 0, st), "launch symcon_bwd_dA_g");
-    else
-      s = cuda_err(cudaLaunchKernel((const void*)p->k_dA, dim3(p->grid_dA), dim3(32 * p->kc.tile_warps), args, p->tile_smem, st),
-                   "launch symcon_bwd_dA");
-    }
+    s = launch_dA_kernel(p, w, q, st);
     if (s) return s;
     n++;
   }
@@ -797,6 +813,12 @@ symcon_status symcon_backward_ex(const symcon_plan* p, int64_t N, const float* A
 symcon_status symcon_backward2(const symcon_plan* p, int64_t N, const float* A, const float* W, const int32_t* ne,
                                const float* dB, const float* uA, float* dB_bar, float* A_bar, float* W_bar, void* ws,
                                size_t ws_bytes, uint32_t flags, void* stream) {
+  return symcon_backward2_ex(p, N, A, W, ne, dB, uA, nullptr, dB_bar, A_bar, W_bar, ws, ws_bytes, flags, stream);
+}
+
+symcon_status symcon_backward2_ex(const symcon_plan* p, int64_t N, const float* A, const float* W, const int32_t* ne,
+                                  const float* dB, const float* uA, const float* uW, float* dB_bar, float* A_bar, float* W_bar,
+                                  void* ws, size_t ws_bytes, uint32_t flags, void* stream) {
   if (!p) { set_error("plan is NULL"); return SYMCON_EINVAL; }
   cudaStream_t st = (cudaStream_t)stream;
   p->last_launches = 0;
@@ -807,7 +829,8 @@ symcon_status symcon_backward2(const symcon_plan* p, int64_t N, const float* A, 
   symcon_status s = check_common(p, N, A, W, ne, ws, ws_bytes);
   if (s) return s;
   if (!dB || !aligned16(dB)) { set_error("dB must be non-NULL and 16-byte aligned"); return SYMCON_EINVAL; }
-  if (!uA || !aligned16(uA)) { set_error("uA must be non-NULL and 16-byte aligned"); return SYMCON_EINVAL; }
+  if (!uA && !uW) { set_error("uA and uW are both NULL"); return SYMCON_EINVAL; }
+  if (uA && !aligned16(uA)) { set_error("uA must be 16-byte aligned"); return SYMCON_EINVAL; }
   if ((dB_bar && !aligned16(dB_bar)) || (A_bar && !aligned16(A_bar))) {
     set_error("dB_bar and A_bar must be 16-byte aligned");
     return SYMCON_EINVAL;
@@ -828,7 +851,15 @@ symcon_status symcon_backward2(const symcon_plan* p, int64_t N, const float* A, 
   int n = launch_prep(p, w, (char*)ws, N, ne, W, q, st, tile, &s, flags);
   if (s) return s;
   void* args[] = {&q};
-  if (W_bar) {
+  if (!uA) {   // only the uW terms: start from zero
+    if (W_bar && (s = cuda_err(cudaMemsetAsync(W_bar, 0, sizeof(float) * (size_t)p->t.E * p->t.paths.size() * p->t.K, st), "memset W_bar")))
+      return s;
+    if (dB_bar && (s = cuda_err(cudaMemsetAsync(dB_bar, 0, sizeof(float) * (size_t)N * p->t.K * p->t.out_per_ch, st), "memset dB_bar")))
+      return s;
+    if (A_bar && (s = cuda_err(cudaMemsetAsync(A_bar, 0, sizeof(float) * (size_t)N * p->t.K * p->t.n_lm, st), "memset A_bar")))
+      return s;
+  }
+  if (W_bar && uA) {
     {
       Timed tm(p, K_BWD2_DW, st);
       s = cuda_err(cudaLaunchKernel((const void*)p->k_bwd2_dW, dim3((unsigned)(w.max_items * p->dw2_nz), (p->t.K + 31) / 32, 1),
@@ -836,13 +867,13 @@ symcon_status symcon_backward2(const symcon_plan* p, int64_t N, const float* A, 
     }
     if (s) return s;
     Timed tm(p, K_UNFOLD, st);
-    n += reduce_items_launch(q.spart, q.item_off, p->t.E, p->npad, p->t.K, q.stot, st);
+    if (!p->kc.unfold_reduce) n += reduce_items_launch(q.spart, q.item_off, p->t.E, p->npad, p->t.K, q.stot, st);
     s = cuda_err(cudaLaunchKernel((const void*)p->k_unfold, dim3(p->t.E, (p->t.K + 31) / 32), dim3(512), args,
                                   p->unfold_smem, st), "launch symcon_unfold");
     if (s) return s;
     n += 2;
   }
-  if (tile) {
+  if (tile && uA) {
     {
       Timed tm(p, K_BWD2, st);
       s = cuda_err(cudaLaunchKernel((const void*)p->k_bwd2, dim3(p->grid_bwd2), dim3(32 * p->kc.tile_warps), args, p->tile_smem, st),
@@ -850,6 +881,33 @@ symcon_status symcon_backward2(const symcon_plan* p, int64_t N, const float* A, 
     }
     if (s) return s;
     n++;
+  }
+  if (tile && uW) {
+    // the cotangent uW of dW: dB_bar += forward(A, uW) and A_bar += dA(A, uW, dB), with uW folded into a
+    // second coefficient table; the kernels add into the outputs (accum)
+    Params q2 = q;
+    q2.W = uW;
+    q2.coef = (float*)((char*)ws + w.coef2);
+    q2.coef_r = (float*)((char*)ws + w.coef_r2);
+    q2.accum = 1;
+    {
+      Timed tm(p, K_FOLD, st);
+      void* a2[] = {&q2};
+      s = cuda_err(cudaLaunchKernel((const void*)p->k_fold, dim3(p->t.E, (p->t.K + 31) / 32, p->kc.fold_split), dim3(128), a2, 0, st),
+                   "launch symcon_fold (uW)");
+    }
+    if (s) return s;
+    n++;
+    if (dB_bar) {
+      q2.B = dB_bar;
+      if ((s = launch_fwd_kernel(p, w, q2, N, st))) return s;
+      n++;
+    }
+    if (A_bar) {
+      q2.dA = A_bar;
+      if ((s = launch_dA_kernel(p, w, q2, st))) return s;
+      n++;
+    }
   }
   p->last_launches = n;
   return cuda_err(cudaGetLastError(), "backward2 launch");

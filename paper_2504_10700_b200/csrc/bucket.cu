@@ -9,6 +9,7 @@
 //   bk_scatter  one warp per chunk, 32 nodes at a time with __match_any_sync ranks: stable
 //   bk_fill_nan writes NaN rows for nodes in the out-of-range bucket
 // All integer work; deterministic for a given node_elem.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -259,8 +260,162 @@ __global__ void bk_fill_nan(const int* __restrict__ perm, const int* __restrict_
   }
 }
 
+// One cooperative launch for the whole bucketing (E + 1 <= kWarpE): CTA b owns 1024-node chunks
+// [b*S, (b+1)*S). Phase 1: per-chunk histograms -> hist. grid sync. Phase 2: every CTA derives the
+// element totals, seg_off and its own chunks' offsets from hist (no second sync); CTA 0 also writes
+// seg_off, the tile / item lists, tile_off / item_off, the padding of tile_perm, the error word and
+// zeroes zero_buf. Phase 3: the block-parallel stable scatter of bk_scatter_blk on each own chunk.
+// Same results as bk_hist + bk_scan + bk_scatter_blk (deterministic, stable).
+__global__ void __launch_bounds__(1024) bk_fused(BucketArgs a, int nchunks, int S) {
+  namespace cg = cooperative_groups;
+  extern __shared__ int sm[];   // h[E+1] | tot[E+1] | base[E+1] | cw[32][E+1]
+  const int E = a.E, E1 = E + 1, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  int* h = sm;
+  int* tot = sm + E1;
+  int* base = sm + 2 * E1;
+  int* cw = sm + 3 * E1;
+  __shared__ int bad;
+  const int c0 = blockIdx.x * S, c1 = min(nchunks, c0 + S);
+  // ---- phase 1: histograms of the own chunks
+  for (int c = c0; c < c1; c++) {
+    for (int e = tid; e <= E; e += blockDim.x) h[e] = 0;
+    if (tid == 0) bad = 0x7fffffff;
+    __syncthreads();
+    const int i = c * 1024 + tid;
+    if (i < a.N) {
+      int e = a.node_elem[i];
+      if (e < 0 || e >= E) { e = E; atomicMin(&bad, i); }
+      atomicAdd(&h[e], 1);
+    }
+    __syncthreads();
+    for (int e = tid; e <= E; e += blockDim.x) a.hist[(size_t)c * E1 + e] = h[e];
+    if (tid == 0) a.chunk_bad[c] = bad;
+    __syncthreads();
+  }
+  cg::this_grid().sync();
+  // ---- phase 2: totals, element offsets (exclusive scan), this CTA's first chunk offset per element
+  for (int e = tid; e <= E; e += blockDim.x) {
+    int t = 0, b = 0;
+    for (int c = 0; c < nchunks; c++) {
+      const int v = __ldcg(a.hist + (size_t)c * E1 + e);
+      if (c < c0) b += v;
+      t += v;
+    }
+    tot[e] = t;
+    base[e] = b;
+  }
+  __syncthreads();
+  if (tid == 0) {   // exclusive scan of totals (E1 <= 512: serial is short)
+    int run = 0;
+    for (int e = 0; e <= E; e++) { const int t = tot[e]; tot[e] = run; run += t; }
+  }
+  __syncthreads();
+  // tot[e] now = seg_off[e]
+  if (blockIdx.x == 0) {
+    if (tid == 0) {
+      int b = 0x7fffffff;
+      for (int c = 0; c < nchunks; c++) b = min(b, __ldcg(a.chunk_bad + c));
+      *a.err = (b == 0x7fffffff) ? ~0ull : (unsigned long long)b;
+      int ts = 0, is = 0;
+      for (int e = 0; e <= E; e++) {
+        const int cnt = (e < E ? tot[e + 1] : a.N) - tot[e];
+        a.seg_off[e] = tot[e];
+        const int nt = (e < E) ? (cnt + a.tile_nodes - 1) / a.tile_nodes : 0;
+        a.tile_off[e] = ts;
+        a.item_off[e] = is;
+        ts += nt;
+        is += (nt + a.tiles_per_item - 1) / a.tiles_per_item;
+      }
+      a.seg_off[E + 1] = a.N;
+      *a.n_tiles = ts;
+      *a.n_items = is;
+      a.item_off[E + 1] = is;
+    }
+    if (a.zero_buf)
+      for (int x = tid; x < a.zero_n; x += blockDim.x) a.zero_buf[x] = 0;
+    __syncthreads();
+    // tiles / items / padding, one warp per element (as bk_scan step 3)
+    for (int e = warp; e < E; e += blockDim.x >> 5) {
+      const int start = tot[e], cnt = tot[e + 1] - tot[e];
+      const int nt = (cnt + a.tile_nodes - 1) / a.tile_nodes, toff = a.tile_off[e], ioff = a.item_off[e];
+      for (int t = lane; t < nt; t += 32) {
+        const int q0 = t * a.tile_nodes;
+        a.tiles[toff + t] = make_int4(e, start + q0, min(a.tile_nodes, cnt - q0), t);
+      }
+      const int ni = (nt + a.tiles_per_item - 1) / a.tiles_per_item;
+      for (int q = lane; q < ni; q += 32) {
+        const int t0 = q * a.tiles_per_item;
+        a.items[ioff + q] = make_int4(e, toff + t0, min(a.tiles_per_item, nt - t0), q);
+      }
+      if (nt > 0)
+        for (int q = cnt - (nt - 1) * a.tile_nodes + lane; q < a.tile_nodes; q += 32)
+          a.tile_perm[(size_t)(toff + nt - 1) * a.tile_nodes + q] = -1;
+    }
+  }
+  // per-element tile offsets for the scatter (every CTA; same arithmetic as CTA 0's list)
+  __syncthreads();
+  if (tid == 0) {
+    int ts = 0;
+    for (int e = 0; e <= E; e++) {
+      const int cnt = (e < E ? tot[e + 1] : a.N) - tot[e];
+      h[e] = ts;   // tile_off (h reused)
+      ts += (e < E) ? (cnt + a.tile_nodes - 1) / a.tile_nodes : 0;
+    }
+  }
+  __syncthreads();
+  // ---- phase 3: stable scatter of the own chunks (bk_scatter_blk)
+  for (int c = c0; c < c1; c++) {
+    for (int x = tid; x < 32 * E1; x += blockDim.x) cw[x] = 0;
+    __syncthreads();
+    const int i = c * 1024 + tid;
+    int e = -1;
+    if (i < a.N) {
+      e = a.node_elem[i];
+      if (e < 0 || e >= E) e = E;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    if (e >= 0 && lane == __ffs(peers) - 1) cw[warp * E1 + e] = __popc(peers);
+    __syncthreads();
+    for (int x = tid; x < E1; x += blockDim.x) {
+      int r = tot[x] + base[x];
+      base[x] += __ldcg(a.hist + (size_t)c * E1 + x);   // next own chunk starts after this one
+#pragma unroll 8
+      for (int w = 0; w < 32; w++) {
+        const int v = cw[w * E1 + x];
+        cw[w * E1 + x] = r;
+        r += v;
+      }
+    }
+    __syncthreads();
+    if (e >= 0) {
+      const int pos = cw[warp * E1 + e] + rank;
+      a.perm[pos] = i;
+      if (e < E) {
+        const int r = pos - tot[e];
+        a.tile_perm[(size_t)(h[e] + r / a.tile_nodes) * a.tile_nodes + r % a.tile_nodes] = i;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 int bucket_launch(const BucketArgs& a, cudaStream_t st) {
   const int nchunks = (a.N + kChunk - 1) / kChunk;
+  if (a.fused && a.N > 0 && a.E + 1 <= kWarpE) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int S = (nchunks + sms - 1) / sms, nb = (nchunks + S - 1) / S;
+    const size_t smem = sizeof(int) * 35 * (size_t)(a.E + 1);
+    static bool attr = false;
+    if (!attr) { cudaFuncSetAttribute(bk_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024); attr = true; }
+    BucketArgs aa = a;
+    int nc = nchunks, ss = S;
+    void* args[] = {&aa, &nc, &ss};
+    if (cudaLaunchCooperativeKernel((const void*)bk_fused, dim3(nb), dim3(1024), args, smem, st) == cudaSuccess) return 1;
+    cudaGetLastError();   // fall back to the three kernels
+  }
   const size_t sm_e = sizeof(int) * (a.E + 1);
   if (a.N > 0) bk_hist<<<nchunks, 256, sm_e, st>>>(a.node_elem, a.N, a.E, a.hist, a.chunk_bad);
   if (3 * sm_e > 48 * 1024) cudaFuncSetAttribute(bk_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * sm_e));

@@ -86,6 +86,16 @@ struct KernelConfig {
   int dw_r_block = 8;        // dw_r: nodes per shared-memory block
   int dw_r_minb = 0;         // dw_r: __launch_bounds__ min blocks
   int dw_r_unroll = 1;       // dw_r: node-loop unroll
+  int fwd_r_nst = 2;         // fwd_r: TMA ring stages
+  int dw_r_nst = 2;          // dw_r: TMA ring stages
+  int dbg_nomem = 0;         // timing experiment only: dw_r without its loads (wrong results)
+  int dw_r_split = 1;        // dw_r: warps per output slot (each takes a balanced range of first indices a)
+  int bucket_fused = 0;      // element bucketing as one cooperative kernel (bk_fused)
+  int fwd_r_tr = 0;          // fwd_r: interleave the block's node pairs once in shared memory (no per-warp pairing)
+  int unfold_reduce = 0;     // the unfold kernel sums the element's dW item partials itself (no dw_reduce_items)
+  int fwd_r_npw = 1;         // fwd_r: node pairs per warp iteration (1 or 2)
+  int r_rotate = 1;          // fwd_r / dW_r: rotate the warp -> output slot map by CTA
+  int fold_split = 4;        // W-fold: CTAs per (element, 32-channel block) (grid.z)
   int dw_r_fuse = 0;         // dw_r: the last CTA of each (element, channel block) reduces + unfolds in-kernel
   int da_s = -1;             // dA as symcon_bwd_dA_s (one node per lane, scalar FP32); -1 auto
   int da_s_warps = 4;        // da_s: warps (channels) per CTA

@@ -24,6 +24,7 @@ struct BucketArgs {
   unsigned long long* err;
   int* zero_buf;   // zeroed by bk_scan (dW_r per-(element, channel block) item counters), may be NULL
   int zero_n;
+  int fused;       // one cooperative kernel (bk_fused) instead of bk_hist + bk_scan + bk_scatter
 };
 
 int bucket_launch(const BucketArgs& a, cudaStream_t st);   // returns launches issued
@@ -58,6 +59,8 @@ struct TPCsrArgs {
   int* send_pos;            // [E] position of edge e in the sender CSR (inverse of send_perm)
 };
 int tp_csr_launch(const TPCsrArgs& a, cudaStream_t st);
+// dst[i] += src[i] for i < n (dst, src 16-byte aligned)
+int add_inplace_launch(float* dst, const float* src, long long n, cudaStream_t st);
 int tp_dh_reduce_launch(const float* dhe, const int* off, const int* perm, int N, int K, int nh, float* dh,
                         cudaStream_t st);
 

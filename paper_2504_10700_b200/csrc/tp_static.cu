@@ -201,4 +201,23 @@ int tp_dh_reduce_launch(const float* dhe, const int* off, const int* perm, int N
   return 1;
 }
 
+// dst[i] += src[i] (the sums of the TP double backward's passes, symcon_tp_backward2)
+__global__ void add_inplace(float* __restrict__ dst, const float* __restrict__ src, long long n) {
+  const long long n4 = n / 4;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    float4 a = reinterpret_cast<float4*>(dst)[i];
+    const float4 b = reinterpret_cast<const float4*>(src)[i];
+    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    reinterpret_cast<float4*>(dst)[i] = a;
+  }
+  for (long long i = 4 * n4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    dst[i] += src[i];
+}
+
+int add_inplace_launch(float* dst, const float* src, long long n, cudaStream_t st) {
+  if (n <= 0) return 0;
+  add_inplace<<<grid_for((n + 3) / 4, 256), 256, 0, st>>>(dst, src, n);
+  return 1;
+}
+
 }  // namespace symcon

@@ -98,21 +98,26 @@ class SymmetricContraction:
         return (dA if need_dA else None), (dW if need_dW else None)
 
     def backward2_raw(self, A, W, node_elem, dB, uA, need_dB=True, need_A=True, need_W=True, ws_key="default",
-                      reuse=False, W_bar=None):
-        """Double backward: (dB_bar, A_bar, W_bar) = derivatives of <uA, dA(A, W, dB)> (symcon_backward2).
-        W_bar may be given (e.g. a symmetric buffer for the peer all-reduce)."""
+                      reuse=False, W_bar=None, uW=None):
+        """Double backward: (dB_bar, A_bar, W_bar) = derivatives of <uA, dA(A, W, dB)> + <uW, dW(A, dB)>
+        (symcon_backward2_ex; uA or uW may be None). W_bar may be given (e.g. a symmetric buffer for the
+        peer all-reduce)."""
         N = self._check(A, W, node_elem)
         assert dB.dtype == torch.float32 and dB.is_contiguous() and dB.shape == (N, self.out_dim)
-        assert uA.dtype == torch.float32 and uA.is_contiguous() and uA.shape == A.shape
+        assert uA is not None or uW is not None
+        if uA is not None:
+            assert uA.dtype == torch.float32 and uA.is_contiguous() and uA.shape == A.shape
+        if uW is not None:
+            assert uW.dtype == torch.float32 and uW.is_contiguous() and uW.shape == W.shape
         dBb = torch.empty_like(dB) if need_dB else None
         Ab = torch.empty_like(A) if need_A else None
         Wb = (W_bar if W_bar is not None else torch.empty_like(W)) if need_W else None
         ws = self.workspace(N, ws_key)
         flags = (_lib.SYMCON_REUSE_BUCKETS | _lib.SYMCON_REUSE_FOLD) if reuse else 0
         ptr = lambda x: x.data_ptr() if x is not None else None
-        _lib.symcon_backward2(self.plan, N, A.data_ptr(), W.data_ptr(), node_elem.data_ptr(), dB.data_ptr(),
-                              uA.data_ptr(), ptr(dBb), ptr(Ab), ptr(Wb), ws.data_ptr(), ws.numel(), flags,
-                              _stream_ptr(self.device))
+        _lib.symcon_backward2_ex(self.plan, N, A.data_ptr(), W.data_ptr(), node_elem.data_ptr(), dB.data_ptr(),
+                                 ptr(uA), ptr(uW), ptr(dBb), ptr(Ab), ptr(Wb), ws.data_ptr(), ws.numel(), flags,
+                                 _stream_ptr(self.device))
         return dBb, Ab, Wb
 
     def check_device_error(self, ws_key="default"):
@@ -150,8 +155,8 @@ class _SymconFn(torch.autograd.Function):
 
 
 class _SymconBwdFn(torch.autograd.Function):
-    """(A, W, dB) -> (dA, dW) with its own backward: the uA terms run in symcon_backward2; the uW
-    terms are the forward (dB_bar += B(A, uW)) and the dA backward (A_bar += dA(A, uW, dB))."""
+    """(A, W, dB) -> (dA, dW) with its own backward: the uA terms (symcon_backward2 kernels) and the uW
+    terms (dB_bar += B(A, uW), A_bar += dA(A, uW, dB)) in one symcon_backward2_ex call."""
 
     @staticmethod
     def forward(ctx, A, W, node_elem, dB, sc):
@@ -166,17 +171,13 @@ class _SymconBwdFn(torch.autograd.Function):
         A, W, node_elem, dB = ctx.saved_tensors
         sc = ctx.sc
         need_A, need_W, need_dB = ctx.needs_input_grad[0], ctx.needs_input_grad[1], ctx.needs_input_grad[3]
-        A_bar = W_bar = dB_bar = None
-        if uA is not None and (need_A or need_W or need_dB):
-            dB_bar, A_bar, W_bar = sc.backward2_raw(A, W, node_elem, dB, uA.contiguous(), need_dB, need_A, need_W)
-        if uW is not None and (need_A or need_dB):
-            uW = uW.contiguous()
-            if need_dB:
-                f = sc.forward_raw(A, uW, node_elem)
-                dB_bar = f if dB_bar is None else dB_bar.add_(f)
-            if need_A:
-                a, _ = sc.backward_raw(A, uW, node_elem, dB, need_dW=False)
-                A_bar = a if A_bar is None else A_bar.add_(a)
+        uA = uA.contiguous() if uA is not None else None
+        uW = uW.contiguous() if uW is not None else None
+        need_W = need_W and uA is not None          # W_bar has no uW term (dW does not depend on W)
+        if (uA is None and uW is None) or not (need_A or need_W or need_dB):
+            return None, None, None, None, None
+        # uA and uW terms are summed inside libsymcon (symcon_backward2_ex): no arithmetic here
+        dB_bar, A_bar, W_bar = sc.backward2_raw(A, W, node_elem, dB, uA, need_dB, need_A, need_W, uW=uW)
         return A_bar, W_bar, None, dB_bar, None
 
 
@@ -241,6 +242,21 @@ class ChannelwiseTP:
                                 ptr(dY), ptr(dh), ptr(dR), ws.data_ptr(), ws.numel(), _stream_ptr(self.device))
         return dY, dh, dR
 
+    def backward2_raw(self, Y, h, R, sender, receiver, dA, uY, uh, uR):
+        """(Y_bar, h_bar, R_bar, dA_bar): the TP double backward (symcon_tp_backward2), returned in the
+        order of _TPBwdFn's inputs (Y, h, R, [sender, receiver,] dA)."""
+        N, E = self._check(Y, h, R, sender, receiver)
+        dA_bar = torch.empty((N, self.channels, self.n_out), dtype=torch.float32, device=self.device)
+        Yb, hb, Rb = torch.empty_like(Y), torch.empty_like(h), torch.empty_like(R)
+        nbytes = _lib.symcon_tp_workspace2_bytes(self.plan, N, E)
+        ws2 = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+        ws2[:8].fill_(255)
+        ptr = lambda t: t.data_ptr() if (t is not None and t.numel()) else None
+        _lib.symcon_tp_backward2(self.plan, N, E, ptr(Y), ptr(h), ptr(R), ptr(sender), ptr(receiver), dA.contiguous().data_ptr(),
+                                 ptr(uY), ptr(uh), ptr(uR), dA_bar.data_ptr(), ptr(Yb), ptr(hb), ptr(Rb), ws2.data_ptr(),
+                                 ws2.numel(), _stream_ptr(self.device))
+        return Yb, hb, Rb, None, None, dA_bar
+
     def check_device_error(self):
         if self._ws is None:
             return 0, -1
@@ -290,11 +306,7 @@ class _TPBwdFn(torch.autograd.Function):
     def backward(ctx, uY, uh, uR):
         Y, h, R, s, r, dA = ctx.saved_tensors
         tp = ctx.tp
-        z = lambda x, ref: torch.zeros_like(ref) if x is None else x.contiguous()
+        z = lambda x, ref: torch.zeros_like(ref) if x is None else x.contiguous()   # absent cotangent = 0
         uY, uh, uR = z(uY, Y), z(uh, h), z(uR, R)
-        dA_bar = tp.forward_raw(uY, h, R, s, r)
-        dA_bar.add_(tp.forward_raw(Y, uh, R, s, r)).add_(tp.forward_raw(Y, h, uR, s, r))
-        a_Y, _, a_R = tp.backward_raw(Y, uh, R, s, r, dA, True, False, True)    # h := uh
-        b_Y, b_h, _ = tp.backward_raw(Y, h, uR, s, r, dA, True, True, False)    # R := uR
-        _, c_h, c_R = tp.backward_raw(uY, h, R, s, r, dA, False, True, True)    # Y := uY
-        return a_Y.add_(b_Y), b_h.add_(c_h), a_R.add_(c_R), None, None, dA_bar, None
+        # all six passes and their sums run in libsymcon (symcon_tp_backward2)
+        return tp.backward2_raw(Y, h, R, s, r, dA, uY, uh, uR) + (None,)

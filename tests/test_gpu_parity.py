@@ -441,3 +441,35 @@ def test_backward2_full_size_sampled(config):
     assert abs(lhs - rhs) <= 1e-5 * (W.double().abs() * Wb.double().abs()).sum().item()
     del A, dB, uA, dBb, Ab
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("name,lmax,corr,outs,E,K,N,with_uA", [
+    ("mp_shape_uW_only", 3, 3, (0, 1), 89, 128, 2000, False),
+    ("mp_shape_uA_uW", 3, 3, (0, 1), 89, 128, 2000, True),
+    ("off_shape_uA_uW", 3, 3, (0,), 10, 96, 1500, True),
+    ("large_shape_uW_only", 3, 3, (0, 1, 2), 89, 256, 400, False),
+])
+def test_backward2_ex_uW_terms_in_library(name, lmax, corr, outs, E, K, N, with_uA):
+    """symcon_backward2_ex: the cotangent uW of dW adds dB_bar += forward(A, uW) and A_bar += dA(A, uW, dB)
+    inside libsymcon (second fold + accumulating forward / dA kernels), no caller arithmetic."""
+    from oracle.contraction import Problem
+    from oracle.ceval import OracleC
+    sc = _sc(lmax, corr, outs, E, K)
+    A, W, ne, dB = _inputs(sc, N, "zipf", seed=5)
+    uA = _uA(sc, N, 5) if with_uA else None
+    uW = torch.randn(W.shape, generator=torch.Generator("cuda").manual_seed(8), device="cuda")
+    dBb, Ab, Wb = sc.backward2_raw(A, W, ne, dB, uA, uW=uW)
+    torch.cuda.synchronize()
+    assert sc.check_device_error()[0] == 0
+    oc = OracleC(Problem(lmax, corr, outs))
+    hA, hW, hne, hdB, huW = _host(A, W, ne, dB, uW)
+    dB_ref = oc.forward(hA, huW, hne)
+    A_ref = oc.backward(hA, huW, hne, hdB, want_dW=False)[0]
+    if with_uA:
+        r = oc.backward2(hA, hW, hne, hdB, uA.cpu().numpy())
+        dB_ref, A_ref = dB_ref + r[0], A_ref + r[1]
+        assert _rel(Wb.cpu(), r[2]) < TOL
+    else:
+        assert torch.count_nonzero(Wb) == 0
+    assert _rel(dBb.cpu(), dB_ref) < TOL, name
+    assert _rel(Ab.cpu(), A_ref) < TOL, name
