@@ -69,8 +69,12 @@ typedef struct {
   int64_t n_fold;        /* (L,M,monomial) rows: folded coefficients per (element, channel) */
   int64_t n_monomials;   /* distinct monomials of A used */
   int32_t device;        /* -1: host-only plan (tables, no kernels) */
-  int32_t reserved;
+  int32_t reserved;      /* the plan's dtype (SYMCON_F32 / SYMCON_F64) */
 } symcon_info;
+
+/* Arithmetic type of a plan (symcon_build_tables_ex). */
+#define SYMCON_F32 0
+#define SYMCON_F64 1
 
 /* Build the U tables for (lmax_in, correlation, out_L[0..n_out)) and, if device >= 0,
  * generate, compile (NVRTC, sm_100a; cached on disk) and load the kernels for that device.
@@ -80,6 +84,15 @@ typedef struct {
  * On success *plan is owned by the caller and must be freed with symcon_destroy. */
 symcon_status symcon_build_tables(int lmax_in, int correlation, const int* out_L, int n_out,
                                   int num_elements, int channels, int device, symcon_plan** plan);
+
+/* The same with the arithmetic type: SYMCON_F32 (the fp32 kernels; every call below) or SYMCON_F64
+ * (the paper's Float64 runs): every float array of the
+ * forward / backward is double and the calls are symcon_forward_f64 / symcon_backward_f64 (same
+ * layouts, workspace from symcon_workspace_bytes of the fp64 plan). The double backward and the
+ * peer all-reduce are fp32 only. symcon_info.reserved reports the plan's dtype. */
+symcon_status symcon_build_tables_ex(int lmax_in, int correlation, const int* out_L, int n_out,
+                                     int num_elements, int channels, int device, int32_t dtype,
+                                     symcon_plan** plan);
 
 symcon_status symcon_plan_info(const symcon_plan* plan, symcon_info* info);
 
@@ -111,6 +124,16 @@ symcon_status symcon_forward(const symcon_plan* plan, int64_t num_nodes, const f
 symcon_status symcon_backward(const symcon_plan* plan, int64_t num_nodes, const float* A,
                               const float* W, const int32_t* node_elem, const float* dB, float* dA,
                               float* dW, void* ws, size_t ws_bytes, void* stream /* cudaStream_t */);
+
+/* fp64 plans (SYMCON_F64): forward and backward on double arrays, same semantics and layouts as
+ * symcon_forward / symcon_backward_ex (flags: SYMCON_REUSE_*). An fp32 plan returns EINVAL. */
+symcon_status symcon_forward_f64(const symcon_plan* plan, int64_t num_nodes, const double* A,
+                                 const double* W, const int32_t* node_elem, double* B, void* ws,
+                                 size_t ws_bytes, void* stream /* cudaStream_t */);
+symcon_status symcon_backward_f64(const symcon_plan* plan, int64_t num_nodes, const double* A,
+                                  const double* W, const int32_t* node_elem, const double* dB, double* dA,
+                                  double* dW, void* ws, size_t ws_bytes, uint32_t flags,
+                                  void* stream /* cudaStream_t */);
 
 /* Reuse hints for symcon_backward_ex (a training step calls forward then backward with the
  * same node_elem and W on the same workspace):
@@ -171,6 +194,8 @@ int32_t symcon_profile_read(const symcon_plan* plan, const char** names, int64_t
  * cubin cache and report its path; copy a plan's generated CUDA source (NULL buf: size). */
 symcon_status symcon_precompile(int lmax_in, int correlation, const int* out_L, int n_out, char* path,
                                 size_t path_len);
+symcon_status symcon_precompile_ex(int lmax_in, int correlation, const int* out_L, int n_out, int32_t dtype,
+                                   char* path, size_t path_len);
 size_t symcon_plan_source(const symcon_plan* plan, char* buf, size_t len);
 
 void symcon_destroy(symcon_plan* plan);

@@ -27,7 +27,9 @@ EXPORTS = ["symcon_build_tables", "symcon_plan_info", "symcon_plan_path", "symco
            "symcon_tp_workspace_bytes", "symcon_tp_forward", "symcon_tp_backward", "symcon_tp_check_device_error",
            "symcon_tp_last_launch_count", "symcon_tp_source", "symcon_tp_destroy", "symcon_peer_allreduce",
            "symcon_tp_precompile", "symcon_peer_allreduce_dev", "symcon_peer_allreduce_ex", "symcon_peer_check",
-           "symcon_peer_allreduce_emulate", "symcon_backward2_ex", "symcon_tp_backward2", "symcon_tp_workspace2_bytes"]
+           "symcon_peer_allreduce_emulate", "symcon_backward2_ex", "symcon_tp_backward2", "symcon_tp_workspace2_bytes",
+           "symcon_build_tables_ex", "symcon_forward_f64", "symcon_backward_f64", "symcon_precompile_ex"]
+SYMCON_F32, SYMCON_F64 = 0, 1
 
 
 class SymconInfo(ctypes.Structure):
@@ -100,6 +102,42 @@ def symcon_build_tables(lmax_in, correlation, out_L, num_elements, channels, dev
     check(lib.symcon_build_tables(lmax_in, correlation, arr, len(out_L), num_elements, channels, device,
                                   ctypes.byref(plan)), "symcon_build_tables")
     return plan
+
+
+lib.symcon_build_tables_ex.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_int, ctypes.c_int, _i32, ctypes.POINTER(_vp)]
+lib.symcon_build_tables_ex.restype = ctypes.c_int
+lib.symcon_forward_f64.argtypes = [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
+lib.symcon_forward_f64.restype = ctypes.c_int
+lib.symcon_backward_f64.argtypes = [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, ctypes.c_uint32, _vp]
+lib.symcon_backward_f64.restype = ctypes.c_int
+lib.symcon_precompile_ex.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.c_int, _i32,
+                                     ctypes.c_char_p, _sz]
+lib.symcon_precompile_ex.restype = ctypes.c_int
+
+
+def symcon_build_tables_ex(lmax_in, correlation, out_L, num_elements, channels, device, dtype):
+    arr = (ctypes.c_int * len(out_L))(*out_L)
+    plan = _vp()
+    check(lib.symcon_build_tables_ex(lmax_in, correlation, arr, len(out_L), num_elements, channels, device, dtype,
+                                     ctypes.byref(plan)), "symcon_build_tables_ex")
+    return plan
+
+
+def symcon_forward_f64(plan, num_nodes, A, W, node_elem, B, ws, ws_bytes, stream):
+    check(lib.symcon_forward_f64(plan, num_nodes, A, W, node_elem, B, ws, ws_bytes, stream), "symcon_forward_f64")
+
+
+def symcon_backward_f64(plan, num_nodes, A, W, node_elem, dB, dA, dW, ws, ws_bytes, flags, stream):
+    check(lib.symcon_backward_f64(plan, num_nodes, A, W, node_elem, dB, dA, dW, ws, ws_bytes, flags, stream),
+          "symcon_backward_f64")
+
+
+def symcon_precompile_ex(lmax_in, correlation, out_L, dtype):
+    arr = (ctypes.c_int * len(out_L))(*out_L)
+    buf = ctypes.create_string_buffer(4096)
+    check(lib.symcon_precompile_ex(lmax_in, correlation, arr, len(out_L), dtype, buf, 4096), "symcon_precompile_ex")
+    return buf.value.decode()
 
 
 def symcon_plan_info(plan):

@@ -16,7 +16,7 @@ CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-SOURCES = ["cg.cpp", "builder.cpp", "codegen.cpp", "pack.cpp", "api.cpp", "tp.cpp", "bucket.cu", "tp_static.cu", "peer.cu"]
+SOURCES = ["cg.cpp", "builder.cpp", "codegen.cpp", "codegen_f64.cpp", "pack.cpp", "api.cpp", "tp.cpp", "bucket.cu", "tp_static.cu", "peer.cu"]
 
 # (lmax_in, correlation, out_L): BASELINE configs + the corr-1/2 cases the tests use
 PRESETS = [(3, 3, (0,)), (3, 3, (0, 1)), (3, 3, (0, 1, 2)), (3, 1, (0, 1, 2, 3)), (3, 2, (0,)),
@@ -78,18 +78,25 @@ def precompile_tp(presets=TP_PRESETS):
             raise RuntimeError(f"tp precompile {ly},{hid},{lo},{k} failed: {lib.symcon_last_error().decode()}")
 
 
-def precompile(presets=PRESETS):
+# fp64 plans (SYMCON_F64) compiled at build time: the BASELINE shapes and the fp64 test configurations
+PRESETS_F64 = [(3, 3, (0,)), (3, 3, (0, 1)), (3, 3, (0, 1, 2)), (2, 2, (0, 1))]
+
+
+def precompile(presets=PRESETS, presets_f64=PRESETS_F64):
     lib = ctypes.CDLL(build())
-    lib.symcon_precompile.restype = ctypes.c_int
+    lib.symcon_precompile_ex.restype = ctypes.c_int
+    lib.symcon_precompile_ex.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_int32,
+                                         ctypes.c_char_p, ctypes.c_size_t]
     lib.symcon_last_error.restype = ctypes.c_char_p
     paths = []
-    for lmax, corr, outs in presets:
-        arr = (ctypes.c_int * len(outs))(*outs)
-        buf = ctypes.create_string_buffer(4096)
-        s = lib.symcon_precompile(lmax, corr, arr, len(outs), buf, 4096)
-        if s != 0:
-            raise RuntimeError(f"precompile {lmax},{corr},{outs} failed: {lib.symcon_last_error().decode()}")
-        paths.append(buf.value.decode())
+    for dtype, plist in ((0, presets), (1, presets_f64)):
+        for lmax, corr, outs in plist:
+            arr = (ctypes.c_int * len(outs))(*outs)
+            buf = ctypes.create_string_buffer(4096)
+            s = lib.symcon_precompile_ex(lmax, corr, arr, len(outs), dtype, buf, 4096)
+            if s != 0:
+                raise RuntimeError(f"precompile {lmax},{corr},{outs} dtype {dtype} failed: {lib.symcon_last_error().decode()}")
+            paths.append(buf.value.decode())
     return paths
 
 

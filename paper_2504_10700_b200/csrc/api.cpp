@@ -47,6 +47,7 @@ struct symcon_plan {
   cudaKernel_t k_fwd_r = nullptr;                      // output-slot warps, Horner (kc.fwd_r)
   cudaKernel_t k_dW_r = nullptr;                       // output-slot warps, q-form (kc.dw_r)
   cudaKernel_t k_dA_s = nullptr;                       // one node per lane, scalar (kc.da_s)
+  cudaKernel_t k_reduce64 = nullptr;                   // fp64 plans: the dW item reduction
   size_t da_s_smem = 0;
   int grid_dA_s = 0;
   size_t dw_r_smem = 0;
@@ -164,8 +165,11 @@ struct WsLayout {
 
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
+size_t esz(const symcon_plan* p) { return p->t.f64 ? sizeof(double) : sizeof(float); }
+
 WsLayout layout(const symcon_plan* p, int64_t N) {
   WsLayout w{};
+  const size_t fs = esz(p);
   const int E = p->t.E, K = p->t.K;
   const size_t nch = bucket_chunks(N);
   w.max_tiles = N / p->kc.tile_nodes + E + 1;
@@ -185,9 +189,9 @@ WsLayout layout(const symcon_plan* p, int64_t N) {
   w.item_off = take(sizeof(int) * (E + 2));
   w.tile_off = take(sizeof(int) * (E + 2));
   w.tile_perm = take(sizeof(int) * (size_t)w.max_tiles * p->kc.tile_nodes);
-  w.coef = take(sizeof(float) * (size_t)E * K * p->npad);
-  w.spart = take(sizeof(float) * (size_t)w.max_items * K * p->npad);
-  w.stot = take(sizeof(float) * (size_t)E * K * p->npad);
+  w.coef = take(fs * (size_t)E * K * p->npad);
+  w.spart = take(fs * (size_t)w.max_items * K * p->npad);
+  w.stot = take(fs * (size_t)E * K * p->npad);
   w.coef_r = take(sizeof(float) * (size_t)E * p->t.out_per_ch * std::max(p->rnq, 1) * K * 4);
   w.dw_count = take(sizeof(int) * (size_t)E * ((K + 31) / 32));
   w.coef2 = take(sizeof(float) * (size_t)E * K * p->npad);   // the uW fold of the double backward
@@ -334,7 +338,8 @@ symcon_status symcon_real_cg(int l1, int l2, int L, double* out) {
   return SYMCON_OK;
 }
 
-static symcon_status build_common(int lmax_in, int corr, const int* out_L, int n_out, int E, int K, symcon_plan** out) {
+static symcon_status build_common(int lmax_in, int corr, const int* out_L, int n_out, int E, int K, symcon_plan** out,
+                                  int dtype = SYMCON_F32) {
   symcon_status s = validate_build(lmax_in, corr, out_L, n_out, E, K);
   if (s) return s;
   auto* p = new (std::nothrow) symcon_plan();
@@ -389,17 +394,32 @@ static symcon_status build_common(int lmax_in, int corr, const int* out_L, int n
   if (p->t.n_lm != 16) p->kc.dw_r = 0;
   if (p->kc.da_s < 0) p->kc.da_s = 0;
   if (p->kc.dw_r_block < 2 || 64 % p->kc.dw_r_block) { set_error("bad dw_r_block"); delete p; return SYMCON_EINVAL; }
-  p->source = generate_source(p->t, p->kc);
+  p->t.f64 = dtype == SYMCON_F64;
+  if (p->t.f64) {   // fp64: the plain scalar kernels of codegen_f64.cpp
+    p->kc.fwd_r = p->kc.dw_r = p->kc.da_s = 0;
+    p->kc.gamma = 0;
+    p->kc.fold_split = 1;
+    p->kc.unfold_reduce = 0;
+    p->source = generate_source_f64(p->t, p->kc);
+  } else {
+    p->source = generate_source(p->t, p->kc);
+  }
   *out = p;
   return SYMCON_OK;
 }
 
 symcon_status symcon_build_tables(int lmax_in, int correlation, const int* out_L, int n_out, int num_elements,
                                   int channels, int device, symcon_plan** plan) {
+  return symcon_build_tables_ex(lmax_in, correlation, out_L, n_out, num_elements, channels, device, SYMCON_F32, plan);
+}
+
+symcon_status symcon_build_tables_ex(int lmax_in, int correlation, const int* out_L, int n_out, int num_elements,
+                                     int channels, int device, int32_t dtype, symcon_plan** plan) {
   if (!plan) { set_error("plan is NULL"); return SYMCON_EINVAL; }
   *plan = nullptr;
+  if (dtype != SYMCON_F32 && dtype != SYMCON_F64) { set_error("dtype must be SYMCON_F32 or SYMCON_F64"); return SYMCON_EINVAL; }
   symcon_plan* p = nullptr;
-  symcon_status s = build_common(lmax_in, correlation, out_L, n_out, num_elements, channels, &p);
+  symcon_status s = build_common(lmax_in, correlation, out_L, n_out, num_elements, channels, &p, dtype);
   if (s) return s;
   p->device = device;
   if (device >= 0) {
@@ -421,6 +441,24 @@ symcon_status symcon_build_tables(int lmax_in, int correlation, const int* out_L
     std::vector<char> cubin;
     if (!get_cubin(p->source, cubin, nullptr)) { cudaSetDevice(prev); delete p; return SYMCON_ECUDA; }
     s = cuda_err(cudaLibraryLoadData(&p->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0), "cudaLibraryLoadData");
+    if (!s && p->t.f64) {   // fp64 plan: fold, fwd, dA, dW, reduce64, unfold (codegen_f64.cpp)
+      if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_fold, p->lib, "symcon_fold"), "get symcon_fold");
+      if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_fwd, p->lib, "symcon_fwd"), "get symcon_fwd");
+      if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_dA, p->lib, "symcon_bwd_dA"), "get symcon_bwd_dA");
+      if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_dW, p->lib, "symcon_bwd_dW"), "get symcon_bwd_dW");
+      if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_unfold, p->lib, "symcon_unfold"), "get symcon_unfold");
+      if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_reduce64, p->lib, "symcon_reduce64"), "get symcon_reduce64");
+      int sms = 0, occ_f = 0, occ_a = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+      if (!s) s = cuda_err(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, (const void*)p->k_fwd, 128, 0), "occupancy fwd");
+      if (!s) s = cuda_err(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, (const void*)p->k_dA, 128, 0), "occupancy dA");
+      p->grid_fwd = sms * std::max(occ_f, 1);
+      p->grid_dA = sms * std::max(occ_a, 1);
+      cudaSetDevice(prev);
+      if (s) { if (p->lib) cudaLibraryUnload(p->lib); delete p; return s; }
+      *plan = p;
+      return SYMCON_OK;
+    }
     if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_fold, p->lib, "symcon_fold"), "get symcon_fold");
     if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_fwd, p->lib, "symcon_fwd"), "get symcon_fwd");
     if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_dA, p->lib, "symcon_bwd_dA"), "get symcon_bwd_dA");
@@ -515,8 +553,13 @@ symcon_status symcon_build_tables(int lmax_in, int correlation, const int* out_L
 /* Compile (NVRTC, sm_100a) the kernels for a configuration into the cubin cache without a
  * device (used by the build step on CPU-only hosts). Writes the cubin path if path != NULL. */
 symcon_status symcon_precompile(int lmax_in, int correlation, const int* out_L, int n_out, char* path, size_t path_len) {
+  return symcon_precompile_ex(lmax_in, correlation, out_L, n_out, SYMCON_F32, path, path_len);
+}
+
+symcon_status symcon_precompile_ex(int lmax_in, int correlation, const int* out_L, int n_out, int32_t dtype, char* path,
+                                   size_t path_len) {
   symcon_plan* p = nullptr;
-  symcon_status s = build_common(lmax_in, correlation, out_L, n_out, 1, 1, &p);
+  symcon_status s = build_common(lmax_in, correlation, out_L, n_out, 1, 1, &p, dtype);
   if (s) return s;
   std::vector<char> cubin;
   std::string cp;
@@ -560,6 +603,7 @@ symcon_status symcon_plan_info(const symcon_plan* p, symcon_info* info) {
   info->n_fold = (int64_t)t.rows.size();
   info->n_monomials = t.n_monomials;
   info->device = p->device;
+  info->reserved = p->t.f64 ? SYMCON_F64 : SYMCON_F32;   // dtype
   return SYMCON_OK;
 }
 
@@ -692,6 +736,11 @@ after_bucket:
 // the forward kernel of the plan (fwd_r / gamma / persistent) with the coefficients q.coef(_r) already folded
 static symcon_status launch_fwd_kernel(const symcon_plan* p, const WsLayout& w, Params& q, int64_t N, cudaStream_t st) {
   symcon_status s = SYMCON_OK;
+  if (p->t.f64) {
+    void* args[] = {&q};
+    Timed tm(p, K_FWD, st);
+    return cuda_err(cudaLaunchKernel((const void*)p->k_fwd, dim3(p->grid_fwd), dim3(128), args, 0, st), "launch symcon_fwd (f64)");
+  }
   if (p->k_fwd_r && (s = encode_a_map(q.tmA, q.A, N, p->t.K, p->t.n_lm))) return s;
   void* args[] = {&q};
   Timed tm(p, K_FWD, st);
@@ -709,6 +758,8 @@ static symcon_status launch_fwd_kernel(const symcon_plan* p, const WsLayout& w, 
 static symcon_status launch_dA_kernel(const symcon_plan* p, const WsLayout& w, Params& q, cudaStream_t st) {
   void* args[] = {&q};
   Timed tm(p, K_DA, st);
+  if (p->t.f64)
+    return cuda_err(cudaLaunchKernel((const void*)p->k_dA, dim3(p->grid_dA), dim3(128), args, 0, st), "launch symcon_bwd_dA (f64)");
   if (p->k_dA_s)
     return cuda_err(cudaLaunchKernel((const void*)p->k_dA_s, dim3(p->grid_dA_s), dim3(32 * p->kc.da_s_warps), args, p->da_s_smem, st),
                     "launch symcon_bwd_dA_s");
@@ -719,8 +770,23 @@ static symcon_status launch_dA_kernel(const symcon_plan* p, const WsLayout& w, P
                   "launch symcon_bwd_dA");
 }
 
+static symcon_status forward_impl(const symcon_plan* p, int64_t N, const float* A, const float* W, const int32_t* ne,
+                                  float* B, void* ws, size_t ws_bytes, void* stream);
+
 symcon_status symcon_forward(const symcon_plan* p, int64_t N, const float* A, const float* W, const int32_t* ne,
                              float* B, void* ws, size_t ws_bytes, void* stream) {
+  if (p && p->t.f64) { set_error("fp64 plan: use symcon_forward_f64"); return SYMCON_EINVAL; }
+  return forward_impl(p, N, A, W, ne, B, ws, ws_bytes, stream);
+}
+
+symcon_status symcon_forward_f64(const symcon_plan* p, int64_t N, const double* A, const double* W, const int32_t* ne,
+                                 double* B, void* ws, size_t ws_bytes, void* stream) {
+  if (p && !p->t.f64) { set_error("fp32 plan: use symcon_forward"); return SYMCON_EINVAL; }
+  return forward_impl(p, N, (const float*)A, (const float*)W, ne, (float*)B, ws, ws_bytes, stream);
+}
+
+static symcon_status forward_impl(const symcon_plan* p, int64_t N, const float* A, const float* W, const int32_t* ne,
+                                  float* B, void* ws, size_t ws_bytes, void* stream) {
   symcon_status s = check_common(p, N, A, W, ne, ws, ws_bytes);
   if (s) return s;
   p->last_launches = 0;
@@ -743,20 +809,39 @@ symcon_status symcon_forward(const symcon_plan* p, int64_t N, const float* A, co
   return cuda_err(cudaGetLastError(), "forward launch");
 }
 
+static symcon_status backward_impl(const symcon_plan* p, int64_t N, const float* A, const float* W, const int32_t* ne,
+                                   const float* dB, float* dA, float* dW, void* ws, size_t ws_bytes, uint32_t flags,
+                                   void* stream);
+
 symcon_status symcon_backward(const symcon_plan* p, int64_t N, const float* A, const float* W, const int32_t* ne,
                               const float* dB, float* dA, float* dW, void* ws, size_t ws_bytes, void* stream) {
   return symcon_backward_ex(p, N, A, W, ne, dB, dA, dW, ws, ws_bytes, 0u, stream);
 }
 
+symcon_status symcon_backward_f64(const symcon_plan* p, int64_t N, const double* A, const double* W, const int32_t* ne,
+                                  const double* dB, double* dA, double* dW, void* ws, size_t ws_bytes, uint32_t flags,
+                                  void* stream) {
+  if (p && !p->t.f64) { set_error("fp32 plan: use symcon_backward_ex"); return SYMCON_EINVAL; }
+  return backward_impl(p, N, (const float*)A, (const float*)W, ne, (const float*)dB, (float*)dA, (float*)dW, ws, ws_bytes,
+                       flags, stream);
+}
+
 symcon_status symcon_backward_ex(const symcon_plan* p, int64_t N, const float* A, const float* W, const int32_t* ne,
                                  const float* dB, float* dA, float* dW, void* ws, size_t ws_bytes, uint32_t flags,
                                  void* stream) {
+  if (p && p->t.f64) { set_error("fp64 plan: use symcon_backward_f64"); return SYMCON_EINVAL; }
+  return backward_impl(p, N, A, W, ne, dB, dA, dW, ws, ws_bytes, flags, stream);
+}
+
+static symcon_status backward_impl(const symcon_plan* p, int64_t N, const float* A, const float* W, const int32_t* ne,
+                                   const float* dB, float* dA, float* dW, void* ws, size_t ws_bytes, uint32_t flags,
+                                   void* stream) {
   if (!p) { set_error("plan is NULL"); return SYMCON_EINVAL; }
   cudaStream_t st = (cudaStream_t)stream;
   p->last_launches = 0;
   if (N == 0) {
     // no nodes: dW must still be overwritten with zeros (reading s12)
-    if (dW) return cuda_err(cudaMemsetAsync(dW, 0, sizeof(float) * (size_t)p->t.E * p->t.paths.size() * p->t.K, st), "memset dW");
+    if (dW) return cuda_err(cudaMemsetAsync(dW, 0, esz(p) * (size_t)p->t.E * p->t.paths.size() * p->t.K, st), "memset dW");
     return SYMCON_OK;
   }
   symcon_status s = check_common(p, N, A, W, ne, ws, ws_bytes);
@@ -778,7 +863,24 @@ symcon_status symcon_backward_ex(const symcon_plan* p, int64_t N, const float* A
   if (dW && p->k_dW_r && (s = encode_a_map(q.tmA, A, N, p->t.K, p->t.n_lm))) return s;
   void* args[] = {&q};
   const unsigned ky = (p->t.K + p->kc.warps_per_cta - 1) / p->kc.warps_per_cta;
-  if (dW) {
+  if (dW && p->t.f64) {   // fp64: S partials (item, row group, channel block), item reduction, unfold
+    {
+      Timed tm(p, K_DW, st);
+      const int ng = ((int)p->t.rows.size() + 47) / 48;   // = codegen_f64 RPG 48
+      s = cuda_err(cudaLaunchKernel((const void*)p->k_dW, dim3((unsigned)w.max_items, ng, (p->t.K + 31) / 32), dim3(32), args, 0, st),
+                   "launch symcon_bwd_dW (f64)");
+    }
+    if (s) return s;
+    Timed tm(p, K_UNFOLD, st);
+    const long long per = (long long)p->npad * p->t.K;
+    s = cuda_err(cudaLaunchKernel((const void*)p->k_reduce64, dim3((unsigned)((per + 255) / 256), p->t.E), dim3(256), args, 0, st),
+                 "launch symcon_reduce64");
+    if (s) return s;
+    s = cuda_err(cudaLaunchKernel((const void*)p->k_unfold, dim3(p->t.E, (p->t.K + 31) / 32), dim3(32), args, 0, st),
+                 "launch symcon_unfold (f64)");
+    if (s) return s;
+    n += 3;
+  } else if (dW) {
     {
     Timed tm(p, K_DW, st);
     if (p->k_dW_r)   // S partials (+ with dw_r_fuse the element's item reduction and the unfold)
@@ -820,6 +922,7 @@ symcon_status symcon_backward2_ex(const symcon_plan* p, int64_t N, const float* 
                                   const float* dB, const float* uA, const float* uW, float* dB_bar, float* A_bar, float* W_bar,
                                   void* ws, size_t ws_bytes, uint32_t flags, void* stream) {
   if (!p) { set_error("plan is NULL"); return SYMCON_EINVAL; }
+  if (p->t.f64) { set_error("the double backward is fp32 only"); return SYMCON_EUNSUPPORTED; }
   cudaStream_t st = (cudaStream_t)stream;
   p->last_launches = 0;
   if (N == 0) {

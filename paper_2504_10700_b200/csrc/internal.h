@@ -39,6 +39,7 @@ struct Tables {
   std::vector<SymRow> rows;          // in codegen order (j index)
   int64_t n_sym_terms = 0;
   int n_monomials = 0;
+  bool f64 = false;                  // fp64 plan (codegen_f64.cpp)
 };
 
 bool build_tables(int lmax_in, int corr, const std::vector<int>& out_L, int E, int K, Tables& t);
@@ -88,7 +89,6 @@ struct KernelConfig {
   int dw_r_unroll = 1;       // dw_r: node-loop unroll
   int fwd_r_nst = 2;         // fwd_r: TMA ring stages
   int dw_r_nst = 2;          // dw_r: TMA ring stages
-  int dbg_nomem = 0;         // timing experiment only: dw_r without its loads (wrong results)
   int dw_r_split = 1;        // dw_r: warps per output slot (each takes a balanced range of first indices a)
   int bucket_fused = 0;      // element bucketing as one cooperative kernel (bk_fused)
   int fwd_r_tr = 0;          // fwd_r: interleave the block's node pairs once in shared memory (no per-warp pairing)
@@ -102,6 +102,7 @@ struct KernelConfig {
   int da_s_minb = 0;         // da_s: __launch_bounds__ min blocks
 };
 std::string generate_source(const Tables& t, const KernelConfig& kc);
+std::string generate_source_f64(const Tables& t, const KernelConfig& kc);   // codegen_f64.cpp
 
 // Horner program of one output slot (symcon_fwd_r)
 struct HornerB { int b, row_ab; std::vector<std::pair<int, int>> cs; };   // (c, row j) of degree-3 rows

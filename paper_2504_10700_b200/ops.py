@@ -21,15 +21,19 @@ def _stream_ptr(device):
 class SymmetricContraction:
     """One plan (U tables + loaded sm_100a kernels) per (config, device)."""
 
-    def __init__(self, lmax_in, correlation, out_L, num_elements, channels, device=None):
+    def __init__(self, lmax_in, correlation, out_L, num_elements, channels, device=None, dtype=torch.float32):
         if not torch.cuda.is_available():
             raise RuntimeError("SymmetricContraction needs a CUDA device (libsymcon has no CPU path)")
+        if dtype not in (torch.float32, torch.float64):
+            raise ValueError("dtype must be torch.float32 or torch.float64")
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
         self.lmax_in, self.correlation, self.out_L = lmax_in, correlation, tuple(out_L)
         self.num_elements, self.channels = num_elements, channels
+        self.dtype = dtype
+        code = _lib.SYMCON_F64 if dtype == torch.float64 else _lib.SYMCON_F32
         with torch.cuda.device(self.device):
-            self.plan = _lib.symcon_build_tables(lmax_in, correlation, list(out_L), num_elements, channels,
-                                                 self.device.index)
+            self.plan = _lib.symcon_build_tables_ex(lmax_in, correlation, list(out_L), num_elements, channels,
+                                                    self.device.index, code)
         info = _lib.symcon_plan_info(self.plan)
         self.info = info
         self.n_paths = info.n_paths
@@ -64,9 +68,9 @@ class SymmetricContraction:
 
     def _check(self, A, W, node_elem):
         N = A.shape[0]
-        assert A.is_cuda and A.device == self.device and A.dtype == torch.float32 and A.is_contiguous()
+        assert A.is_cuda and A.device == self.device and A.dtype == self.dtype and A.is_contiguous()
         assert A.shape == (N, self.channels, self.n_lm), A.shape
-        assert W.dtype == torch.float32 and W.is_contiguous() and W.shape == (self.num_elements, self.n_paths, self.channels)
+        assert W.dtype == self.dtype and W.is_contiguous() and W.shape == (self.num_elements, self.n_paths, self.channels)
         assert node_elem.dtype == torch.int32 and node_elem.is_contiguous() and node_elem.shape == (N,)
         return N
 
@@ -74,10 +78,11 @@ class SymmetricContraction:
     def forward_raw(self, A, W, node_elem, B=None, ws_key="default"):
         N = self._check(A, W, node_elem)
         if B is None:
-            B = torch.empty((N, self.out_dim), dtype=torch.float32, device=self.device)
+            B = torch.empty((N, self.out_dim), dtype=self.dtype, device=self.device)
         ws = self.workspace(N, ws_key)
-        _lib.symcon_forward(self.plan, N, A.data_ptr(), W.data_ptr(), node_elem.data_ptr(), B.data_ptr(),
-                            ws.data_ptr(), ws.numel(), _stream_ptr(self.device))
+        fn = _lib.symcon_forward_f64 if self.dtype == torch.float64 else _lib.symcon_forward
+        fn(self.plan, N, A.data_ptr(), W.data_ptr(), node_elem.data_ptr(), B.data_ptr(),
+           ws.data_ptr(), ws.numel(), _stream_ptr(self.device))
         return B
 
     def backward_raw(self, A, W, node_elem, dB, need_dA=True, need_dW=True, dA=None, dW=None, ws_key="default",
@@ -85,16 +90,17 @@ class SymmetricContraction:
         """reuse=True passes SYMCON_REUSE_BUCKETS|FOLD: the bucketing and W-fold left in the
         workspace by the preceding forward (same node_elem / W tensors) are reused."""
         N = self._check(A, W, node_elem)
-        assert dB.dtype == torch.float32 and dB.is_contiguous() and dB.shape == (N, self.out_dim)
+        assert dB.dtype == self.dtype and dB.is_contiguous() and dB.shape == (N, self.out_dim)
         if need_dA and dA is None:
             dA = torch.empty_like(A)
         if need_dW and dW is None:
             dW = torch.empty_like(W)
         ws = self.workspace(N, ws_key)
         flags = (_lib.SYMCON_REUSE_BUCKETS | _lib.SYMCON_REUSE_FOLD) if reuse else 0
-        _lib.symcon_backward_ex(self.plan, N, A.data_ptr(), W.data_ptr(), node_elem.data_ptr(), dB.data_ptr(),
-                                dA.data_ptr() if need_dA else None, dW.data_ptr() if need_dW else None,
-                                ws.data_ptr(), ws.numel(), flags, _stream_ptr(self.device))
+        fn = _lib.symcon_backward_f64 if self.dtype == torch.float64 else _lib.symcon_backward_ex
+        fn(self.plan, N, A.data_ptr(), W.data_ptr(), node_elem.data_ptr(), dB.data_ptr(),
+           dA.data_ptr() if need_dA else None, dW.data_ptr() if need_dW else None,
+           ws.data_ptr(), ws.numel(), flags, _stream_ptr(self.device))
         return (dA if need_dA else None), (dW if need_dW else None)
 
     def backward2_raw(self, A, W, node_elem, dB, uA, need_dB=True, need_A=True, need_W=True, ws_key="default",
