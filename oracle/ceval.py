@@ -40,7 +40,7 @@ class OracleC:
             off += 2 * L + 1
         for p in prob.paths:
             for M, ts, u in p.terms:
-                tp = list(ts) + [0] * (3 - len(ts))
+                tp = list(ts) + [0] * (4 - len(ts))   # up to nu = 4 (correlation 4, reading s4b)
                 rows.append((p.col, p.nu, tp, blk[p.L], 2 * p.L + 1, M + p.L, u))
         self._arr = {
             "col": np.array([r[0] for r in rows], np.int32),

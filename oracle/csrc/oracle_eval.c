@@ -9,7 +9,7 @@
  *
  * Term table (one row per raw nonzero U entry, built by oracle/ceval.py):
  *   col[t]    W column (path)
- *   nu[t]     order 1..3                tup[3t..3t+2] lm indices
+ *   nu[t]     order 1..4                tup[4t..4t+3] lm indices (unused slots 0)
  *   u[t]      U value
  * Output addressing: B[i*out_dim + blk[t]*K + k*wid[t] + mpos[t]].
  */
@@ -56,7 +56,7 @@ void oracle_forward(const oracle_tables* T, int64_t N, int64_t K, const float* A
       const float* a = A + (i * K + k) * T->n_lm;
       for (int64_t t = 0; t < T->n_terms; t++) {
         double prod = T->u[t];
-        for (int j = 0; j < T->nu[t]; j++) prod *= (double)a[T->tup[3 * t + j]];
+        for (int j = 0; j < T->nu[t]; j++) prod *= (double)a[T->tup[4 * t + j]];
         double w = (double)W[(z * T->n_paths + T->col[t]) * K + k];
         Bi[T->blk[t] * K + k * T->wid[t] + T->mpos[t]] += w * prod;
       }
@@ -92,7 +92,7 @@ void oracle_backward(const oracle_tables* T, int64_t N, int64_t K, int64_t E, co
           double g = (double)dB[i * T->out_per_ch * K + T->blk[t] * K + k * T->wid[t] + T->mpos[t]];
           double w = (double)W[(z * T->n_paths + T->col[t]) * K + k];
           int nu = T->nu[t];
-          const int32_t* tp = T->tup + 3 * t;
+          const int32_t* tp = T->tup + 4 * t;
           if (myW) {
             double prod = T->u[t];
             for (int j = 0; j < nu; j++) prod *= (double)a[tp[j]];
@@ -154,7 +154,7 @@ void oracle_backward2(const oracle_tables* T, int64_t N, int64_t K, int64_t E, c
           double g = (double)dB[o];
           double w = (double)W[(z * T->n_paths + T->col[t]) * K + k];
           int nu = T->nu[t];
-          const int32_t* tp = T->tup + 3 * t;
+          const int32_t* tp = T->tup + 4 * t;
           double jvp = 0.0;
           for (int j = 0; j < nu; j++) {
             double part = (double)ua[tp[j]];

@@ -5,9 +5,17 @@ nu = 1..nu_max, over "all combinations lm of l1m1, ..., l_nu m_nu" weighted by
 the generalized Clebsch-Gordan coefficient C^{LM}_{lm} (symbol only,
 PAPER.md:306, 562). Reading s4: C^{LM}_{lm} is a left-nested
 chain of pairwise real couplings (l1 (x) l2 -> L2, L2 (x) l3 -> L3, ...), every
-intermediate allowed, last intermediate = L; a path is kept iff
+intermediate allowed for nu <= 3, last intermediate = L; a path is kept iff
 sum(l) + L is even (natural parity, reading s9). One weight per path eta
 (reading s5): W[z, (L, nu, eta), k].
+
+Reading s4b (nu = 4, correlation 4; SURVEY.md §8(c) s4 "corr-4 mid-filter"): the intermediates of a
+nu = 4 chain are restricted to natural-parity irreps, L_j + l_1 + ... + l_j even at every coupling
+step, L_j < 12 (MACE's filter_ir_mid for correlation 4). The paper's "all possible combinations ...
+that would result in a nonzero contribution" holds: the filter keeps the complete
+invariant space, pinned by the symmetrized rank = the multiplicity of L in Sym^4(0e+1o+2e+3o)
+(23, 31, 46 for L = 0, 1, 2; tests/test_oracle_paths.py) with 158 / 284 / 358 of the 204 / 520 / 720
+unfiltered chains.
 
 eta order inside (L, nu): lexicographic on the interleaved key
 (l1, l2, L2, l3, L3, ...).
@@ -54,6 +62,8 @@ def enumerate_paths(lmax_in, nu, L):
             nxt = []
             for key, cur, mids in stack:
                 for Lj in _tri(cur, ls[j]):
+                    if nu == 4 and ((Lj + sum(ls[:j + 1])) % 2 or Lj >= 12):
+                        continue   # reading s4b: natural-parity intermediates at nu = 4
                     nxt.append((key + (ls[j], Lj), Lj, mids + (Lj,)))
             stack = nxt
         for key, cur, mids in stack:
