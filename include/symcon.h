@@ -47,7 +47,7 @@ extern "C" {
 typedef enum {
   SYMCON_OK = 0,
   SYMCON_EINVAL = 1,       /* bad argument (null pointer, size, alignment, range) */
-  SYMCON_EUNSUPPORTED = 2, /* valid but not supported (e.g. correlation > 3) */
+  SYMCON_EUNSUPPORTED = 2, /* valid but not supported (e.g. correlation > 4) */
   SYMCON_ECUDA = 3,        /* CUDA / NVRTC failure */
   SYMCON_ENOMEM = 4,       /* host allocation or workspace too small */
   SYMCON_EELEMENT = 5,     /* node_elem value outside [0, E) found on the device */
@@ -78,8 +78,11 @@ typedef struct {
 
 /* Build the U tables for (lmax_in, correlation, out_L[0..n_out)) and, if device >= 0,
  * generate, compile (NVRTC, sm_100a; cached on disk) and load the kernels for that device.
- *   lmax_in in [0,3]; correlation in [1,3]; out_L strictly increasing, each in [0,3],
+ *   lmax_in in [0,3]; correlation in [1,4]; out_L strictly increasing, each in [0,3],
  *   n_out in [1,4]; num_elements >= 1; channels >= 1.
+ *   Correlation 4 ("all possible combinations" at nu = 4; reading s4b: every
+ *   nu = 4 intermediate has natural parity and L_j < 12) builds the plain scalar kernels of any
+ *   degree (fp32 or fp64); the double backward (symcon_backward2*) is correlation <= 3 only.
  *   device = -1 builds host tables only (for inspection; compute calls return EINVAL).
  * On success *plan is owned by the caller and must be freed with symcon_destroy. */
 symcon_status symcon_build_tables(int lmax_in, int correlation, const int* out_L, int n_out,
@@ -102,9 +105,14 @@ symcon_status symcon_plan_path(const symcon_plan* plan, int64_t col, int32_t* L,
                                int32_t* eta, int32_t* ls, int32_t* mids);
 
 /* Copy the symmetrised table (host): rows (L, M, monomial a<=b<=c padded with -1, path
- * column, value). Pass NULL arrays to query the count into *n. Used by table-parity tests. */
+ * column, value). Pass NULL arrays to query the count into *n. Used by table-parity tests.
+ * A correlation-4 plan returns EUNSUPPORTED when mono3 is requested (use symcon_plan_sym_table4). */
 symcon_status symcon_plan_sym_table(const symcon_plan* plan, int64_t* n, int32_t* L, int32_t* M,
                                     int32_t* mono3, int32_t* col, double* value);
+
+/* The same with 4 monomial indices per row (a<=b<=c<=d padded with -1): mono4[4 * n]. */
+symcon_status symcon_plan_sym_table4(const symcon_plan* plan, int64_t* n, int32_t* L, int32_t* M,
+                                     int32_t* mono4, int32_t* col, double* value);
 
 /* Copy the pairwise real coupling C^L_{l1 l2}[M][m1][m2] (host) into out
  * [(2L+1)(2l1+1)(2l2+1)] (zeros if the triangle rule fails). l1,l2 <= 3, L <= 6. */

@@ -19,7 +19,7 @@ lib = ctypes.CDLL(LIB_PATH)
 
 SYMCON_OK, SYMCON_EINVAL, SYMCON_EUNSUPPORTED, SYMCON_ECUDA, SYMCON_ENOMEM, SYMCON_EELEMENT, SYMCON_ETIMEOUT = range(7)
 
-EXPORTS = ["symcon_build_tables", "symcon_plan_info", "symcon_plan_path", "symcon_plan_sym_table", "symcon_real_cg",
+EXPORTS = ["symcon_build_tables", "symcon_plan_info", "symcon_plan_path", "symcon_plan_sym_table", "symcon_plan_sym_table4", "symcon_real_cg",
            "symcon_workspace_bytes", "symcon_forward", "symcon_backward", "symcon_backward_ex", "symcon_backward2", "symcon_check_device_error",
            "symcon_last_launch_count", "symcon_destroy", "symcon_status_string", "symcon_last_error",
            "symcon_pack_balanced", "symcon_precompile", "symcon_plan_source", "symcon_profile_enable",
@@ -47,6 +47,7 @@ lib.symcon_build_tables.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(c
 lib.symcon_plan_info.argtypes = [_vp, ctypes.POINTER(SymconInfo)]
 lib.symcon_plan_path.argtypes = [_vp, _i64] + [ctypes.POINTER(_i32)] * 5
 lib.symcon_plan_sym_table.argtypes = [_vp, ctypes.POINTER(_i64), _vp, _vp, _vp, _vp, _vp]
+lib.symcon_plan_sym_table4.argtypes = [_vp, ctypes.POINTER(_i64), _vp, _vp, _vp, _vp, _vp]
 lib.symcon_real_cg.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp]
 lib.symcon_workspace_bytes.argtypes = [_vp, _i64]
 lib.symcon_workspace_bytes.restype = _sz
@@ -75,8 +76,8 @@ lib.symcon_profile_reset.argtypes = [_vp]
 lib.symcon_profile_read.argtypes = [_vp, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(_i64),
                                     ctypes.POINTER(ctypes.c_double)]
 lib.symcon_profile_read.restype = _i32
-for _n in ("symcon_profile_enable", "symcon_profile_reset", "symcon_build_tables", "symcon_plan_info", "symcon_plan_path", "symcon_plan_sym_table", "symcon_real_cg",
-           "symcon_forward", "symcon_backward", "symcon_backward_ex", "symcon_backward2", "symcon_check_device_error", "symcon_pack_balanced",
+for _n in ("symcon_profile_enable", "symcon_profile_reset", "symcon_build_tables", "symcon_plan_info", "symcon_plan_path", "symcon_plan_sym_table", "symcon_plan_sym_table4",
+           "symcon_real_cg", "symcon_forward", "symcon_backward", "symcon_backward_ex", "symcon_backward2", "symcon_check_device_error", "symcon_pack_balanced",
            "symcon_precompile"):
     getattr(lib, _n).restype = ctypes.c_int
 
@@ -148,23 +149,25 @@ def symcon_plan_info(plan):
 
 def symcon_plan_path(plan, col):
     L, nu, eta = _i32(), _i32(), _i32()
-    ls, mids = (_i32 * 3)(), (_i32 * 2)()
+    ls, mids = (_i32 * 4)(), (_i32 * 3)()
     check(lib.symcon_plan_path(plan, col, ctypes.byref(L), ctypes.byref(nu), ctypes.byref(eta), ls, mids),
           "symcon_plan_path")
     return L.value, nu.value, eta.value, tuple(ls[:nu.value]), tuple(mids[:max(nu.value - 1, 0)])
 
 
-def symcon_plan_sym_table(plan):
+def symcon_plan_sym_table(plan, width=3):
+    """(L, M, mono[n, width], col, value); width 4 calls symcon_plan_sym_table4 (correlation 4)."""
     import numpy as np
+    fn = lib.symcon_plan_sym_table if width == 3 else lib.symcon_plan_sym_table4
     n = _i64(0)
-    check(lib.symcon_plan_sym_table(plan, ctypes.byref(n), None, None, None, None, None), "symcon_plan_sym_table")
+    check(fn(plan, ctypes.byref(n), None, None, None, None, None), "symcon_plan_sym_table")
     L = np.zeros(n.value, np.int32)
     M = np.zeros(n.value, np.int32)
-    mono = np.zeros((n.value, 3), np.int32)
+    mono = np.zeros((n.value, width), np.int32)
     col = np.zeros(n.value, np.int32)
     val = np.zeros(n.value, np.float64)
-    check(lib.symcon_plan_sym_table(plan, ctypes.byref(n), L.ctypes.data, M.ctypes.data, mono.ctypes.data,
-                                    col.ctypes.data, val.ctypes.data), "symcon_plan_sym_table")
+    check(fn(plan, ctypes.byref(n), L.ctypes.data, M.ctypes.data, mono.ctypes.data, col.ctypes.data, val.ctypes.data),
+          "symcon_plan_sym_table")
     return L, M, mono, col, val
 
 

@@ -16,7 +16,7 @@ CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-SOURCES = ["cg.cpp", "builder.cpp", "codegen.cpp", "codegen_f64.cpp", "pack.cpp", "api.cpp", "tp.cpp", "bucket.cu", "tp_static.cu", "peer.cu"]
+SOURCES = ["cg.cpp", "builder.cpp", "codegen.cpp", "codegen_simple.cpp", "pack.cpp", "api.cpp", "tp.cpp", "bucket.cu", "tp_static.cu", "peer.cu"]
 
 # (lmax_in, correlation, out_L): BASELINE configs + the corr-1/2 cases the tests use
 PRESETS = [(3, 3, (0,)), (3, 3, (0, 1)), (3, 3, (0, 1, 2)), (3, 1, (0, 1, 2, 3)), (3, 2, (0,)),
@@ -79,10 +79,13 @@ def precompile_tp(presets=TP_PRESETS):
 
 
 # fp64 plans (SYMCON_F64) compiled at build time: the BASELINE shapes and the fp64 test configurations
-PRESETS_F64 = [(3, 3, (0,)), (3, 3, (0, 1)), (3, 3, (0, 1, 2)), (2, 2, (0, 1))]
+PRESETS_F64 = [(3, 3, (0,)), (3, 3, (0, 1)), (3, 3, (0, 1, 2)), (2, 2, (0, 1)),
+               (3, 4, (0,)), (2, 4, (0, 1))]
+# correlation 4 (plain scalar kernels, codegen_simple.cpp; NVRTC ~100 s for (3, 4, (0, 1)))
+PRESETS_C4 = [(3, 4, (0,)), (3, 4, (0, 1)), (2, 4, (0, 1, 2))]
 
 
-def precompile(presets=PRESETS, presets_f64=PRESETS_F64):
+def precompile(presets=PRESETS + PRESETS_C4, presets_f64=PRESETS_F64):
     lib = ctypes.CDLL(build())
     lib.symcon_precompile_ex.restype = ctypes.c_int
     lib.symcon_precompile_ex.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_int32,

@@ -39,6 +39,7 @@ struct symcon_plan {
   int grid_fwd = 0, grid_dA = 0, grid_bwd2 = 0, grid_fwd_r = 0;
   int rnq = 0;                 // fwd_r: coefficient quads per output slot
   size_t fwd_r_smem = 0;
+  size_t simple_smem = 0;                               // simple plans: dynamic smem of fwd / dA
   std::string source;
   cudaLibrary_t lib = nullptr;
   cudaKernel_t k_fold = nullptr, k_fwd = nullptr, k_dA = nullptr, k_dW = nullptr, k_unfold = nullptr;
@@ -47,7 +48,7 @@ struct symcon_plan {
   cudaKernel_t k_fwd_r = nullptr;                      // output-slot warps, Horner (kc.fwd_r)
   cudaKernel_t k_dW_r = nullptr;                       // output-slot warps, q-form (kc.dw_r)
   cudaKernel_t k_dA_s = nullptr;                       // one node per lane, scalar (kc.da_s)
-  cudaKernel_t k_reduce64 = nullptr;                   // fp64 plans: the dW item reduction
+  cudaKernel_t k_reduce_s = nullptr;                   // simple plans (fp64 / corr 4): the dW item reduction
   size_t da_s_smem = 0;
   int grid_dA_s = 0;
   size_t dw_r_smem = 0;
@@ -296,7 +297,7 @@ bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 symcon_status validate_build(int lmax_in, int corr, const int* out_L, int n_out, int E, int K) {
   if (lmax_in < 0 || lmax_in > 3) { set_error("lmax_in must be in [0,3]"); return SYMCON_EINVAL; }
   if (corr < 1) { set_error("correlation must be >= 1"); return SYMCON_EINVAL; }
-  if (corr > 3) { set_error("correlation > 3 is not supported (needs the intermediate-irrep filter)"); return SYMCON_EUNSUPPORTED; }
+  if (corr > 4) { set_error("correlation must be <= 4"); return SYMCON_EUNSUPPORTED; }
   if (!out_L || n_out < 1 || n_out > 4) { set_error("n_out must be in [1,4]"); return SYMCON_EINVAL; }
   for (int i = 0; i < n_out; i++) {
     if (out_L[i] < 0 || out_L[i] > 3) { set_error("out_L values must be in [0,3]"); return SYMCON_EINVAL; }
@@ -356,6 +357,8 @@ static symcon_status build_common(int lmax_in, int corr, const int* out_L, int n
   std::vector<int> ol(out_L, out_L + n_out);
   if (!build_tables(lmax_in, corr, ol, E, K, p->t)) { delete p; return SYMCON_EINVAL; }
   p->npad = (int)((p->t.rows.size() + 31) / 32 * 32);
+  p->t.f64 = dtype == SYMCON_F64;
+  p->t.simple = p->t.f64 || corr == 4;
   // measured defaults (profiles/r01): few large row groups when the dB row is short (MP-medium:
   // 52 rows x 8 warps, fewer smem reads per FMA), smaller groups for the 9-output large shape
   if (p->kc.dw_rows_per_group <= 0) p->kc.dw_rows_per_group = p->t.out_per_ch > 4 ? 56 : 52;
@@ -383,7 +386,7 @@ static symcon_status build_common(int lmax_in, int corr, const int* out_L, int n
     delete p;
     return SYMCON_EINVAL;
   }
-  if (p->kc.fwd_r) {
+  if (p->kc.fwd_r && !p->t.simple) {
     for (auto& h : horner_slots(p->t)) p->rnq = std::max(p->rnq, (int)((h.rows.size() + 3) / 4));
     if (p->t.n_lm != 16) p->kc.fwd_r = 0;   // the A staging is laid out for 16 floats per (node, channel) (lmax_in 3)
   }
@@ -394,13 +397,20 @@ static symcon_status build_common(int lmax_in, int corr, const int* out_L, int n
   if (p->t.n_lm != 16) p->kc.dw_r = 0;
   if (p->kc.da_s < 0) p->kc.da_s = 0;
   if (p->kc.dw_r_block < 2 || 64 % p->kc.dw_r_block) { set_error("bad dw_r_block"); delete p; return SYMCON_EINVAL; }
-  p->t.f64 = dtype == SYMCON_F64;
-  if (p->t.f64) {   // fp64: the plain scalar kernels of codegen_f64.cpp
+  if (p->t.simple) {   // fp64 or correlation 4: the plain scalar kernels of codegen_simple.cpp
     p->kc.fwd_r = p->kc.dw_r = p->kc.da_s = 0;
     p->kc.gamma = 0;
-    p->kc.fold_split = 1;
+    // table-driven fold / unfold: split rows / columns over grid.z (~256 per CTA)
+    p->kc.fold_split = std::min(16, std::max(1, p->npad / 256));
+    p->kc.simple_unfold_split = std::min(16, std::max(1, (int)p->t.paths.size() / 64));
+    // coefficient rows of the SWPC warps of a fwd / dA CTA in dynamic shared memory (<= 200 KB)
+    const size_t row_bytes = esz(p) * (size_t)p->npad;
+    p->kc.simple_warps = 4;
+    while (p->kc.simple_warps > 1 && row_bytes * p->kc.simple_warps > 200 * 1024) p->kc.simple_warps--;
+    if (row_bytes > 200 * 1024) { set_error("folded table too large for shared memory"); delete p; return SYMCON_EUNSUPPORTED; }
+    p->simple_smem = row_bytes * p->kc.simple_warps;
     p->kc.unfold_reduce = 0;
-    p->source = generate_source_f64(p->t, p->kc);
+    p->source = generate_source_simple(p->t, p->kc);
   } else {
     p->source = generate_source(p->t, p->kc);
   }
@@ -441,17 +451,22 @@ symcon_status symcon_build_tables_ex(int lmax_in, int correlation, const int* ou
     std::vector<char> cubin;
     if (!get_cubin(p->source, cubin, nullptr)) { cudaSetDevice(prev); delete p; return SYMCON_ECUDA; }
     s = cuda_err(cudaLibraryLoadData(&p->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0), "cudaLibraryLoadData");
-    if (!s && p->t.f64) {   // fp64 plan: fold, fwd, dA, dW, reduce64, unfold (codegen_f64.cpp)
+    if (!s && p->t.simple) {   // simple plan: fold, fwd, dA, dW, reduce_simple, unfold (codegen_simple.cpp)
       if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_fold, p->lib, "symcon_fold"), "get symcon_fold");
       if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_fwd, p->lib, "symcon_fwd"), "get symcon_fwd");
       if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_dA, p->lib, "symcon_bwd_dA"), "get symcon_bwd_dA");
       if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_dW, p->lib, "symcon_bwd_dW"), "get symcon_bwd_dW");
       if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_unfold, p->lib, "symcon_unfold"), "get symcon_unfold");
-      if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_reduce64, p->lib, "symcon_reduce64"), "get symcon_reduce64");
+      if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_reduce_s, p->lib, "symcon_reduce_simple"), "get symcon_reduce_simple");
       int sms = 0, occ_f = 0, occ_a = 0;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-      if (!s) s = cuda_err(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, (const void*)p->k_fwd, 128, 0), "occupancy fwd");
-      if (!s) s = cuda_err(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, (const void*)p->k_dA, 128, 0), "occupancy dA");
+      const int nthr = 32 * p->kc.simple_warps;
+      if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->simple_smem, device),
+                           "smem fwd");
+      if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_dA, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->simple_smem, device),
+                           "smem dA");
+      if (!s) s = cuda_err(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, (const void*)p->k_fwd, nthr, p->simple_smem), "occupancy fwd");
+      if (!s) s = cuda_err(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, (const void*)p->k_dA, nthr, p->simple_smem), "occupancy dA");
       p->grid_fwd = sms * std::max(occ_f, 1);
       p->grid_dA = sms * std::max(occ_a, 1);
       cudaSetDevice(prev);
@@ -619,23 +634,34 @@ symcon_status symcon_plan_path(const symcon_plan* p, int64_t col, int32_t* L, in
   return SYMCON_OK;
 }
 
-symcon_status symcon_plan_sym_table(const symcon_plan* p, int64_t* n, int32_t* L, int32_t* M, int32_t* mono3,
-                                    int32_t* col, double* value) {
+static symcon_status sym_table(const symcon_plan* p, int64_t* n, int32_t* L, int32_t* M, int32_t* mono, int nm, int32_t* col,
+                               double* value) {
   if (!p || !n) { set_error("NULL argument"); return SYMCON_EINVAL; }
-  if (!L && !M && !mono3 && !col && !value) { *n = p->t.n_sym_terms; return SYMCON_OK; }
+  if (!L && !M && !mono && !col && !value) { *n = p->t.n_sym_terms; return SYMCON_OK; }
+  if (mono && nm < p->t.corr) { set_error("correlation-4 plan: use symcon_plan_sym_table4"); return SYMCON_EUNSUPPORTED; }
   if (*n < p->t.n_sym_terms) { *n = p->t.n_sym_terms; set_error("arrays too small"); return SYMCON_ENOMEM; }
   int64_t q = 0;
   for (auto& r : p->t.rows)
     for (auto& cv : r.cols) {
       if (L) L[q] = r.L;
       if (M) M[q] = r.M;
-      if (mono3) for (int j = 0; j < 3; j++) mono3[3 * q + j] = r.mono[j];
+      if (mono) for (int j = 0; j < nm; j++) mono[nm * q + j] = r.mono[j];
       if (col) col[q] = cv.first;
       if (value) value[q] = cv.second;
       q++;
     }
   *n = q;
   return SYMCON_OK;
+}
+
+symcon_status symcon_plan_sym_table(const symcon_plan* p, int64_t* n, int32_t* L, int32_t* M, int32_t* mono3,
+                                    int32_t* col, double* value) {
+  return sym_table(p, n, L, M, mono3, 3, col, value);
+}
+
+symcon_status symcon_plan_sym_table4(const symcon_plan* p, int64_t* n, int32_t* L, int32_t* M, int32_t* mono4,
+                                     int32_t* col, double* value) {
+  return sym_table(p, n, L, M, mono4, 4, col, value);
 }
 
 size_t symcon_workspace_bytes(const symcon_plan* p, int64_t N) {
@@ -736,10 +762,11 @@ after_bucket:
 // the forward kernel of the plan (fwd_r / gamma / persistent) with the coefficients q.coef(_r) already folded
 static symcon_status launch_fwd_kernel(const symcon_plan* p, const WsLayout& w, Params& q, int64_t N, cudaStream_t st) {
   symcon_status s = SYMCON_OK;
-  if (p->t.f64) {
+  if (p->t.simple) {
     void* args[] = {&q};
     Timed tm(p, K_FWD, st);
-    return cuda_err(cudaLaunchKernel((const void*)p->k_fwd, dim3(p->grid_fwd), dim3(128), args, 0, st), "launch symcon_fwd (f64)");
+    return cuda_err(cudaLaunchKernel((const void*)p->k_fwd, dim3(p->grid_fwd), dim3(32 * p->kc.simple_warps), args, p->simple_smem, st),
+                    "launch symcon_fwd (simple)");
   }
   if (p->k_fwd_r && (s = encode_a_map(q.tmA, q.A, N, p->t.K, p->t.n_lm))) return s;
   void* args[] = {&q};
@@ -758,8 +785,9 @@ static symcon_status launch_fwd_kernel(const symcon_plan* p, const WsLayout& w, 
 static symcon_status launch_dA_kernel(const symcon_plan* p, const WsLayout& w, Params& q, cudaStream_t st) {
   void* args[] = {&q};
   Timed tm(p, K_DA, st);
-  if (p->t.f64)
-    return cuda_err(cudaLaunchKernel((const void*)p->k_dA, dim3(p->grid_dA), dim3(128), args, 0, st), "launch symcon_bwd_dA (f64)");
+  if (p->t.simple)
+    return cuda_err(cudaLaunchKernel((const void*)p->k_dA, dim3(p->grid_dA), dim3(32 * p->kc.simple_warps), args, p->simple_smem, st),
+                    "launch symcon_bwd_dA (simple)");
   if (p->k_dA_s)
     return cuda_err(cudaLaunchKernel((const void*)p->k_dA_s, dim3(p->grid_dA_s), dim3(32 * p->kc.da_s_warps), args, p->da_s_smem, st),
                     "launch symcon_bwd_dA_s");
@@ -863,21 +891,21 @@ static symcon_status backward_impl(const symcon_plan* p, int64_t N, const float*
   if (dW && p->k_dW_r && (s = encode_a_map(q.tmA, A, N, p->t.K, p->t.n_lm))) return s;
   void* args[] = {&q};
   const unsigned ky = (p->t.K + p->kc.warps_per_cta - 1) / p->kc.warps_per_cta;
-  if (dW && p->t.f64) {   // fp64: S partials (item, row group, channel block), item reduction, unfold
+  if (dW && p->t.simple) {   // simple plans: S partials (item, row group, channel block), item reduction, unfold
     {
       Timed tm(p, K_DW, st);
-      const int ng = ((int)p->t.rows.size() + 47) / 48;   // = codegen_f64 RPG 48
+      const int ng = ((int)p->t.rows.size() + 47) / 48;   // = codegen_simple RPG 48
       s = cuda_err(cudaLaunchKernel((const void*)p->k_dW, dim3((unsigned)w.max_items, ng, (p->t.K + 31) / 32), dim3(32), args, 0, st),
-                   "launch symcon_bwd_dW (f64)");
+                   "launch symcon_bwd_dW (simple)");
     }
     if (s) return s;
     Timed tm(p, K_UNFOLD, st);
     const long long per = (long long)p->npad * p->t.K;
-    s = cuda_err(cudaLaunchKernel((const void*)p->k_reduce64, dim3((unsigned)((per + 255) / 256), p->t.E), dim3(256), args, 0, st),
-                 "launch symcon_reduce64");
+    s = cuda_err(cudaLaunchKernel((const void*)p->k_reduce_s, dim3((unsigned)((per + 255) / 256), p->t.E), dim3(256), args, 0, st),
+                 "launch symcon_reduce_simple");
     if (s) return s;
-    s = cuda_err(cudaLaunchKernel((const void*)p->k_unfold, dim3(p->t.E, (p->t.K + 31) / 32), dim3(32), args, 0, st),
-                 "launch symcon_unfold (f64)");
+    s = cuda_err(cudaLaunchKernel((const void*)p->k_unfold, dim3(p->t.E, (p->t.K + 31) / 32, p->kc.simple_unfold_split), dim3(128),
+                                  args, 0, st), "launch symcon_unfold (simple)");
     if (s) return s;
     n += 3;
   } else if (dW) {
@@ -922,7 +950,7 @@ symcon_status symcon_backward2_ex(const symcon_plan* p, int64_t N, const float* 
                                   const float* dB, const float* uA, const float* uW, float* dB_bar, float* A_bar, float* W_bar,
                                   void* ws, size_t ws_bytes, uint32_t flags, void* stream) {
   if (!p) { set_error("plan is NULL"); return SYMCON_EINVAL; }
-  if (p->t.f64) { set_error("the double backward is fp32 only"); return SYMCON_EUNSUPPORTED; }
+  if (p->t.simple) { set_error("the double backward is fp32 with correlation <= 3 only"); return SYMCON_EUNSUPPORTED; }
   cudaStream_t st = (cudaStream_t)stream;
   p->last_launches = 0;
   if (N == 0) {

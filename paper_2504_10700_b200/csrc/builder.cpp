@@ -10,7 +10,8 @@
 // 3. Symmetrise to sorted monomials: U~[(L,M,mono), path] = sum over ordered tuples t that
 //    sort to mono of U[M,t]. B only sees U~ because prod_j A[t_j] depends on the multiset.
 // 4. Rows (L,M,mono) are put in codegen order: degree-1 rows, then per prefix (a,b):
-//    the degree-2 row(s) (a,b) followed by degree-3 rows (a,b,c), c ascending.
+//    the degree-2 row(s) (a,b) followed by degree-3 rows (a,b,c), c ascending, each followed by
+//    its degree-4 rows (a,b,c,d), d ascending (correlation 4).
 #include <algorithm>
 #include <cmath>
 #include <map>
@@ -30,24 +31,40 @@ void enumerate(int lmax, int nu, int L, std::vector<PathDesc>& out) {
     }
     return;
   }
+  // nu = 4 (correlation 4, reading s4b): every intermediate L_j has natural parity,
+  // (L_j + l_1 + ... + l_j) even, and L_j <= 11 (the coupling tables stop at 3 + 3 + 3 + 3 - 1)
+  auto nat = [&](int Lj, int s) { return nu < 4 || ((Lj + s) % 2 == 0 && Lj < 12); };
   for (int l1 = 0; l1 <= lmax; l1++)
     for (int l2 = 0; l2 <= lmax; l2++)
       for (int L2 = std::abs(l1 - l2); L2 <= l1 + l2; L2++) {
         if (nu == 2) {
           if (L2 == L && keep(l1 + l2)) {
             PathDesc p;
-            p.L = L; p.nu = 2; p.ls = {l1, l2, -1}; p.mids = {L2, -1};
+            p.L = L; p.nu = 2; p.ls = {l1, l2, -1, -1}; p.mids = {L2, -1, -1};
             out.push_back(p);
           }
           continue;
         }
+        if (!nat(L2, l1 + l2)) continue;
         for (int l3 = 0; l3 <= lmax; l3++)
-          for (int L3 = std::abs(L2 - l3); L3 <= L2 + l3; L3++)
-            if (L3 == L && keep(l1 + l2 + l3)) {
-              PathDesc p;
-              p.L = L; p.nu = 3; p.ls = {l1, l2, l3}; p.mids = {L2, L3};
-              out.push_back(p);
+          for (int L3 = std::abs(L2 - l3); L3 <= L2 + l3; L3++) {
+            if (nu == 3) {
+              if (L3 == L && keep(l1 + l2 + l3)) {
+                PathDesc p;
+                p.L = L; p.nu = 3; p.ls = {l1, l2, l3, -1}; p.mids = {L2, L3, -1};
+                out.push_back(p);
+              }
+              continue;
             }
+            if (!nat(L3, l1 + l2 + l3)) continue;
+            for (int l4 = 0; l4 <= lmax; l4++)
+              for (int L4 = std::abs(L3 - l4); L4 <= L3 + l4; L4++)
+                if (L4 == L && keep(l1 + l2 + l3 + l4)) {
+                  PathDesc p;
+                  p.L = L; p.nu = 4; p.ls = {l1, l2, l3, l4}; p.mids = {L2, L3, L4};
+                  out.push_back(p);
+                }
+          }
       }
 }
 
@@ -78,7 +95,7 @@ bool build_tables(int lmax_in, int corr, const std::vector<int>& out_L, int E, i
       }
     }
   // symmetrised accumulation: key (out index, M, mono) -> col -> value
-  std::map<std::tuple<int, int, std::array<int, 3>>, std::map<int, double>> acc;
+  std::map<std::tuple<int, int, std::array<int, 4>>, std::map<int, double>> acc;
   t.n_raw_terms = 0;
   for (const auto& p : t.paths) {
     int oi = (int)(std::find(out_L.begin(), out_L.end(), p.L) - out_L.begin());
@@ -114,7 +131,7 @@ bool build_tables(int lmax_in, int corr, const std::vector<int>& out_L, int E, i
         double u = T[M * inner + r];
         if (std::abs(u) <= 1e-13) continue;
         t.n_raw_terms++;
-        std::array<int, 3> tup{{-1, -1, -1}};
+        std::array<int, 4> tup{{-1, -1, -1, -1}};
         int rem = r;
         for (int j = p.nu - 1; j >= 0; j--) {
           int nl = 2 * p.ls[j] + 1;
@@ -137,7 +154,7 @@ bool build_tables(int lmax_in, int corr, const std::vector<int>& out_L, int E, i
     s.M = std::get<1>(kv.first);
     s.out = t.out_off[oi] + s.M + s.L;
     s.mono = std::get<2>(kv.first);
-    s.deg = (s.mono[0] >= 0) + (s.mono[1] >= 0) + (s.mono[2] >= 0);
+    s.deg = (s.mono[0] >= 0) + (s.mono[1] >= 0) + (s.mono[2] >= 0) + (s.mono[3] >= 0);
     for (auto& cv : kv.second)
       if (std::abs(cv.second) > 1e-12) s.cols.push_back({cv.first, cv.second});
     if (s.cols.empty()) continue;
@@ -146,14 +163,15 @@ bool build_tables(int lmax_in, int corr, const std::vector<int>& out_L, int E, i
   }
   // codegen order
   auto key = [](const SymRow& s) {
-    // deg-1 first (group -1), then prefix (a,b) groups, inside: deg2 before deg3, c asc
-    int a = s.mono[0], b = s.deg >= 2 ? s.mono[1] : -1, c = s.deg == 3 ? s.mono[2] : -1;
+    // deg-1 first (group -1), then prefix (a,b) groups, inside: deg2 before deg3 (c asc), each
+    // deg-3 row (a,b,c) before its deg-4 extensions (a,b,c,d), d asc (monomials padded with -1)
+    int a = s.mono[0], b = s.deg >= 2 ? s.mono[1] : -1;
     int grp = (s.deg == 1) ? -1 : a * 64 + b;
-    return std::make_tuple(grp, s.deg == 1 ? a : c, s.out);
+    return std::make_tuple(grp, s.deg == 1 ? a : s.mono[2], s.mono[3], s.out);
   };
   std::stable_sort(rows.begin(), rows.end(), [&](const SymRow& x, const SymRow& y) { return key(x) < key(y); });
   t.rows = rows;
-  std::map<std::array<int, 3>, int> monos;
+  std::map<std::array<int, 4>, int> monos;
   for (auto& r : t.rows) monos[r.mono] = 1;
   t.n_monomials = (int)monos.size();
   return true;

@@ -18,14 +18,14 @@ std::vector<double> real_coupling(int l1, int l2, int L);
 // ---- builder.cpp
 struct PathDesc {
   int L, nu, eta, col;
-  std::array<int, 3> ls{{-1, -1, -1}};
-  std::array<int, 2> mids{{-1, -1}};
+  std::array<int, 4> ls{{-1, -1, -1, -1}};
+  std::array<int, 3> mids{{-1, -1, -1}};
 };
 
 struct SymRow {                 // one (L, M, monomial) row of the symmetrised table
   int L, M;                     // output irrep and component (M in [-L, L])
   int out;                      // per-channel output slot: off_L + M + L
-  std::array<int, 3> mono;      // a <= b <= c, padded with -1
+  std::array<int, 4> mono;      // a <= b <= c <= d, padded with -1
   int deg;
   std::vector<std::pair<int, double>> cols;  // (path column, U~ value)
 };
@@ -39,7 +39,8 @@ struct Tables {
   std::vector<SymRow> rows;          // in codegen order (j index)
   int64_t n_sym_terms = 0;
   int n_monomials = 0;
-  bool f64 = false;                  // fp64 plan (codegen_f64.cpp)
+  bool f64 = false;                  // fp64 plan
+  bool simple = false;               // plain scalar kernels of codegen_simple.cpp (fp64, or correlation 4)
 };
 
 bool build_tables(int lmax_in, int corr, const std::vector<int>& out_L, int E, int K, Tables& t);
@@ -100,9 +101,12 @@ struct KernelConfig {
   int da_s = -1;             // dA as symcon_bwd_dA_s (one node per lane, scalar FP32); -1 auto
   int da_s_warps = 4;        // da_s: warps (channels) per CTA
   int da_s_minb = 0;         // da_s: __launch_bounds__ min blocks
+  int simple_warps = 4;      // simple plans (fp64 / corr 4): warps per fwd / dA CTA (coefficient rows in dynamic smem)
+  int simple_unfold_split = 1;  // simple plans: column split of the unfold grid (grid.z)
 };
 std::string generate_source(const Tables& t, const KernelConfig& kc);
-std::string generate_source_f64(const Tables& t, const KernelConfig& kc);   // codegen_f64.cpp
+// codegen_simple.cpp: plain scalar kernels of any degree (prefix-trie forward, reverse-mode dA), fp32 or fp64
+std::string generate_source_simple(const Tables& t, const KernelConfig& kc);
 
 // Horner program of one output slot (symcon_fwd_r)
 struct HornerB { int b, row_ab; std::vector<std::pair<int, int>> cs; };   // (c, row j) of degree-3 rows

@@ -28,8 +28,13 @@ def test_exports_every_declared_symbol(L):
 
 def test_invalid_arguments(L):
     with pytest.raises(L.SymconError) as e:
-        L.symcon_build_tables(3, 4, [0], 2, 8, -1)
+        L.symcon_build_tables(3, 5, [0], 2, 8, -1)
     assert e.value.status == L.SYMCON_EUNSUPPORTED
+    plan4 = L.symcon_build_tables(3, 4, [0], 2, 8, -1)   # correlation 4: mono3 export refused
+    with pytest.raises(L.SymconError) as e:
+        L.symcon_plan_sym_table(plan4)
+    assert e.value.status == L.SYMCON_EUNSUPPORTED
+    L.symcon_destroy(plan4)
     for args in [(4, 3, [0]), (3, 0, [0]), (3, 3, [1, 0]), (3, 3, [])]:
         with pytest.raises(L.SymconError) as e:
             L.symcon_build_tables(args[0], args[1], args[2], 2, 8, -1)
@@ -51,7 +56,7 @@ def test_real_cg_parity_with_oracle(L):
 
 
 @pytest.mark.parametrize("lmax,corr,outs", [(3, 3, (0,)), (3, 3, (0, 1)), (3, 3, (0, 1, 2)), (2, 3, (0, 1)),
-                                            (3, 1, (0, 1, 2, 3)), (3, 2, (1,))])
+                                            (3, 1, (0, 1, 2, 3)), (3, 2, (1,)), (3, 4, (0, 1)), (2, 4, (0, 1, 2))])
 def test_tables_parity_with_oracle(L, lmax, corr, outs):
     from oracle.contraction import Problem
     plan = L.symcon_build_tables(lmax, corr, list(outs), 3, 8, -1)
@@ -62,12 +67,13 @@ def test_tables_parity_with_oracle(L, lmax, corr, outs):
     for c, p in enumerate(prob.paths):
         assert L.symcon_plan_path(plan, c) == (p.L, p.nu, p.eta, p.ls, p.mids)
     acc = {}
+    W = 4 if corr == 4 else 3
     for p in prob.paths:
         for M, ts, u in p.terms:
-            key = (p.L, M, tuple(sorted(ts)) + (-1,) * (3 - len(ts)), p.col)
+            key = (p.L, M, tuple(sorted(ts)) + (-1,) * (W - len(ts)), p.col)
             acc[key] = acc.get(key, 0.0) + u
     acc = {k: v for k, v in acc.items() if abs(v) > 1e-12}
-    Lr, M, mono, col, val = L.symcon_plan_sym_table(plan)
+    Lr, M, mono, col, val = L.symcon_plan_sym_table(plan, W)
     mine = {(int(Lr[i]), int(M[i]), tuple(int(x) for x in mono[i]), int(col[i])): val[i] for i in range(len(val))}
     assert set(mine) == set(acc)
     assert max(abs(mine[k] - acc[k]) for k in acc) < 1e-12

@@ -49,11 +49,25 @@ def traffic(tag, out_dir):
 
         def v(k, table):
             return float(d[k].replace(",", "")) * table.get(units[hdr.index(k)], 1)
-        out[name] = {"dram_bytes_read": v("dram__bytes_read.sum", scale), "dram_bytes_write": v("dram__bytes_write.sum", scale),
-                     "time_us": v("gpu__time_duration.sum", tscale),
-                     "fma_pipe_pct": float(d["sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"]),
-                     "issue_pct": float(d["smsp__issue_active.avg.pct_of_peak_sustained_active"]),
-                     "registers": int(float(d["launch__registers_per_thread"]))}
+        rec = {"dram_bytes_read": v("dram__bytes_read.sum", scale), "dram_bytes_write": v("dram__bytes_write.sum", scale),
+               "time_us": v("gpu__time_duration.sum", tscale),
+               "fma_pipe_pct": float(d["sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"]),
+               "issue_pct": float(d["smsp__issue_active.avg.pct_of_peak_sustained_active"]),
+               "registers": int(float(d["launch__registers_per_thread"]))}
+        # executed FP32 lane-ops (thread instructions; the packed forms do 2 lane-ops each) and local bytes
+        ops = {k: d.get(f"sm__sass_thread_inst_executed_op_{k}_pred_on.sum") for k in ("ffma", "ffma2", "fmul", "fmul2", "fadd", "fadd2")}
+        if all(x not in (None, "") for x in ops.values()):
+            ops = {k: float(x.replace(",", "")) for k, x in ops.items()}
+            rec["thread_inst"] = ops
+            rec["executed_lane_ops"] = ops["ffma"] + ops["fmul"] + ops["fadd"] + 2 * (ops["ffma2"] + ops["fmul2"] + ops["fadd2"])
+        for k, key in (("local_ld_bytes", "sm__sass_data_bytes_mem_local_op_ld.sum"), ("local_st_bytes", "sm__sass_data_bytes_mem_local_op_st.sum")):
+            if d.get(key) not in (None, ""):
+                rec[k] = v(key, scale)
+        out[name] = rec
+        # the bench reports kernels by launch group (symcon_fwd covers symcon_fwd_r, ...)
+        alias = {"symcon_fwd_r": "symcon_fwd", "symcon_bwd_dW_r": "symcon_bwd_dW", "symcon_bwd_dA_s": "symcon_bwd_dA"}.get(name)
+        if alias and alias not in out:
+            out[alias] = dict(rec, kernel=name)
     json.dump({"source": f"ncu --set full --clock-control none, tools/profile_step.py (MP-medium, 50k nodes), capture {tag}",
                "kernels": out}, open(os.path.join(out_dir, "ncu_traffic.json"), "w"), indent=1)
     summ = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), rep], capture_output=True, text=True).stdout

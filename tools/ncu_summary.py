@@ -20,6 +20,13 @@ KEYS = {
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum": "smem_ld_conf",
     "l1tex__t_bytes_pipe_lsu_mem_local_op_ld.sum": "local_ld",
     "launch__grid_size": "grid",
+    "sm__sass_thread_inst_executed_op_ffma_pred_on.sum": "ffma",
+    "sm__sass_thread_inst_executed_op_ffma2_pred_on.sum": "ffma2",
+    "sm__sass_thread_inst_executed_op_fmul_pred_on.sum": "fmul",
+    "sm__sass_thread_inst_executed_op_fmul2_pred_on.sum": "fmul2",
+    "sm__sass_thread_inst_executed_op_fadd_pred_on.sum": "fadd",
+    "sm__sass_data_bytes_mem_local_op_ld.sum": "local_ld_B",
+    "sm__sass_data_bytes_mem_local_op_st.sum": "local_st_B",
 }
 
 
