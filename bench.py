@@ -72,6 +72,11 @@ def parse(argv=None):
     ap.add_argument("--double-backward", action="store_true",
                     help="force-training step (SURVEY §8(f) row 1): fwd + bwd + the double backward "
                          "(dB_bar, A_bar, W_bar of <uA, dA>) per step; metric symcon_fwd_bwd_bwd2_nodes_per_s")
+    ap.add_argument("--dtype", default="f32", choices=["f32", "f64"],
+                    help="arithmetic type of the plan (SURVEY §8(f) row 3: f64 = the paper's Float64 runs, "
+                         "PAPER.md:1063; plain scalar DFMA kernels, NCCL all-reduce at N > 1)")
+    ap.add_argument("--correlation", type=int, default=None, choices=[1, 2, 3, 4],
+                    help="override the config's correlation order (4: reading s4b, plain scalar kernels)")
     a = ap.parse_args(argv)
     if a.capacity is None:
         a.capacity = DEFAULT_CAPACITY[a.config]
@@ -79,9 +84,23 @@ def parse(argv=None):
 
 
 # ----------------------------------------------------------------------------- workload
-def shape_of(name):
+def shape_of(name, correlation=None):
+    import dataclasses
     from synth.inputs import CONFIGS
-    return CONFIGS[name]
+    cfg = CONFIGS[name]
+    return dataclasses.replace(cfg, correlation=correlation) if correlation else cfg
+
+
+def fp64_lanes_per_sm_clk():
+    """DFMA lane-ops per SM clock: measured by tools/probes/dfma_probe.cu (profiles/r02/dfma_probe.jsonl,
+    best variant), else the nominal 64 (B200 FP64 = half the FP32 lane count)."""
+    path = os.path.join(ROOT, "profiles", "r02", "dfma_probe.jsonl")
+    if os.path.exists(path):
+        vals = [json.loads(ln).get("dfma_per_sm_clk_median") for ln in open(path) if ln.startswith("{")]
+        vals = [v for v in vals if v]
+        if vals:
+            return max(vals), "measured (tools/probes/dfma_probe.cu, profiles/r02/dfma_probe.jsonl)"
+    return 64.0, "nominal (64 FP64 lanes per SM)"
 
 
 def plan_bins(world, capacity=CAPACITY, seed=0):
@@ -171,6 +190,8 @@ def alg_ops(sc):
              only its degree-1 row)
       path = fwd + dA + dW (the monomial-first forms, 888 / 888, are reported beside them)."""
     from paper_2504_10700_b200 import _lib
+    if getattr(sc, "correlation", 3) == 4:
+        return alg_ops_trie(sc)
     L, M, mono, col, val = _lib.symcon_plan_sym_table(sc.plan)
     rows = {(int(L[i]), int(M[i]), tuple(int(x) for x in mono[i])) for i in range(len(L))}
     monos = {r[2] for r in rows}
@@ -215,19 +236,52 @@ def alg_ops(sc):
             "n_sym": int(len(L))}
 
 
-def path_roofline(cfg, sc, mean_nodes, path_ops, ms_step, dbl, sm_mhz=1965.0):
+def alg_ops_trie(sc):
+    """alg_ops for any degree (correlation 4), on the monomial prefix trie: forward = Horner per output
+    slot = one FMA per node of the slot's trie; dW = the slot's reverse Horner = one product (or FMA) per
+    trie node + one add per row sitting at an internal node; dA = the reverse of the global trie: one
+    prefix product per internal node at depth >= 2, one op per folded row (g), 2 per node at depth >= 2
+    (D_f += h P, h_parent += h A_f; at depth 2 the parent's share goes straight into D_a), 1 per degree-1
+    monomial (D_a += g). At degree <= 3 these equal alg_ops' formulas exactly."""
+    from paper_2504_10700_b200 import _lib
+    L, M, mono, col, val = _lib.symcon_plan_sym_table(sc.plan, 4)
+    rows = {(int(L[i]), int(M[i]), tuple(int(x) for x in mono[i] if x >= 0)) for i in range(len(L))}
+
+    def trie(ms):
+        nodes = {m[:d] for m in ms for d in range(1, len(m) + 1)}
+        internal = {n[:-1] for n in nodes if len(n) >= 2}
+        return nodes, internal
+    slots = {}
+    for (Lr, Mr, m) in rows:
+        slots.setdefault((Lr, Mr), []).append(m)
+    fwd = dW = 0
+    for ms in slots.values():
+        nodes, internal = trie(ms)
+        fwd += len(nodes)
+        dW += len(nodes) + sum(1 for m in ms if m in internal)
+    monos = {r[2] for r in rows}
+    nodes, internal = trie(monos)
+    n_fold = len(rows)
+    dA = sum(1 for n in internal if len(n) >= 2) + n_fold + 2 * sum(1 for n in nodes if len(n) >= 2) + \
+        sum(1 for m in monos if len(m) == 1)
+    return {"fwd": fwd, "dA": dA, "dW": dW, "path": fwd + dA + dW, "n_fold": n_fold, "monomials": len(monos),
+            "trie_nodes": len(nodes), "n_sym": int(len(L)), "bwd2": 0, "bwd2_dW": 0,
+            "note": "prefix-trie counts (alg_ops_trie); the plain scalar kernels execute the monomial-first forms"}
+
+
+def path_roofline(cfg, sc, mean_nodes, path_ops, ms_step, dbl, sm_mhz=1965.0, esz=4, lanes=128):
     """Whole-step roofline: the step's algorithmic FP32 lane-ops at the ALU peak vs its
     algorithmic HBM bytes at the measured copy bandwidth (A read twice, dB, B and dA
     once per node-channel; the double backward adds uA, A, dB reads and dB_bar, A_bar writes)."""
     K = cfg.channels
     nlm = (cfg.lmax_in + 1) ** 2
     outc = sc.out_dim // K
-    per = 4 * (2 * nlm + outc + outc + nlm)
+    per = esz * (2 * nlm + outc + outc + nlm)
     if dbl:
-        per += 4 * (3 * nlm + outc + outc + nlm)
+        per += esz * (3 * nlm + outc + outc + nlm)
     hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6553.0
-    t_alu = path_ops / (148 * 128 * sm_mhz * 1e6)
+    t_alu = path_ops / (148 * lanes * sm_mhz * 1e6)
     t_hbm = per * mean_nodes * K / (hbm * 1e9)
     bound = "alu" if t_alu >= t_hbm else "hbm"
     return {"bound": bound, "frac": max(t_alu, t_hbm) / (ms_step / 1e3), "t_alu_ms": t_alu * 1e3, "t_hbm_ms": t_hbm * 1e3,
@@ -363,7 +417,7 @@ def run_reference(args):
     from synth.inputs import gen_W
     from oracle.contraction import Problem
     from oracle.ceval import OracleC
-    cfg = shape_of(args.config)
+    cfg = shape_of(args.config, args.correlation)
     prob = Problem(cfg.lmax_in, cfg.correlation, cfg.out_L)
     oc = OracleC(prob)
     world = max(args.gpus, 1)
@@ -410,7 +464,9 @@ def run_reference(args):
 
 def workload_config(args, cfg, nodes_per_bin):
     return {"workload": f"{args.config}_dp_step" + ("_double_backward" if args.double_backward else "")
-                        + ("" if args.capacity == DEFAULT_CAPACITY[args.config] else f"_C{args.capacity}"),
+                        + ("" if args.capacity == DEFAULT_CAPACITY[args.config] else f"_C{args.capacity}")
+                        + (f"_corr{args.correlation}" if args.correlation else "")
+                        + ("_f64" if args.dtype == "f64" else ""),
             "batch": ("20k-node batches of U[10,100]-atom molecules, organic element mix" if args.capacity is None else
                       f"Alg. 1 bins of the Table-2 manifest, capacity {args.capacity} nodes"),
             "model": "MACE symmetric contraction", "channels": cfg.channels,
@@ -429,17 +485,21 @@ class TimedStep:
     against the oracle."""
 
     def __init__(self, config="mp_medium", capacity=CAPACITY, world=1, rank=0, device=0, pool=POOL,
-                 double_backward=False, allreduce="peer", peer_algo=0, overlap=True, concurrent_bwd=None):
+                 double_backward=False, allreduce="peer", peer_algo=0, overlap=True, concurrent_bwd=None,
+                 dtype="f32", correlation=None):
         import torch
         from paper_2504_10700_b200.ops import SymmetricContraction
         from paper_2504_10700_b200.dist import BinPackedShards, DataParallelContraction
         from synth.inputs import gen_A, gen_W, table2_sizes
         self.torch = torch
-        self.cfg = cfg = shape_of(config)
+        self.cfg = cfg = shape_of(config, correlation)
         self.dev = dev = torch.device("cuda", device)
         self.world, self.rank, self.double_backward = world, rank, double_backward
+        self.dtype = tdt = torch.float64 if dtype == "f64" else torch.float32
+        if tdt == torch.float64:
+            allreduce = "nccl"     # the peer all-reduce kernel is fp32
         self.sc = sc = SymmetricContraction(cfg.lmax_in, cfg.correlation, cfg.out_L, cfg.n_elements, cfg.channels,
-                                            device=device)
+                                            device=device, dtype=tdt)
         self.capacity = capacity
         self.pool, self.uA, self.mol_sizes = [], {}, []
         t0 = time.time()
@@ -459,14 +519,15 @@ class TimedStep:
                 msz, ne, A, dB = molecule_batch(cfg, q, rank, sc.out_dim, sc.n_lm, dev)
                 self.mol_sizes.append(msz)
             N = ne.numel()
-            B = torch.empty((N, sc.out_dim), device=dev)
+            A, dB = A.to(tdt), dB.to(tdt)      # same seeded values (drawn in fp32) in the plan's dtype
+            B = torch.empty((N, sc.out_dim), device=dev, dtype=tdt)
             dA = torch.empty_like(A)
             self.pool.append((b, N, A, ne, dB, B, dA))
             if double_backward:
                 self.uA[q] = gen_A(N, cfg.channels, sc.n_lm, dev, seed=100 * q + rank + 7)
         self.imbalance = (max(self.shards.step_imbalance(q % self.shards.n_steps) for q in range(pool))
                           if self.shards is not None else 1.0)
-        self.W = gen_W(cfg.n_elements, sc.block_sizes(), cfg.channels, dev)
+        self.W = gen_W(cfg.n_elements, sc.block_sizes(), cfg.channels, dev).to(tdt)
         if world > 1:
             import torch.distributed as dist
             dist.broadcast(self.W, 0)
@@ -530,10 +591,10 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
     from paper_2504_10700_b200 import _lib
     from paper_2504_10700_b200.dist import DataParallelContraction
-    cfg = shape_of(args.config)
+    cfg = shape_of(args.config, args.correlation)
     conc = False if args.sequential_bwd else (True if args.concurrent_bwd else None)
     ts = TimedStep(args.config, args.capacity, world, rank, local, POOL, args.double_backward, args.allreduce,
-                   args.peer_algo, not args.no_overlap, conc)
+                   args.peer_algo, not args.no_overlap, conc, args.dtype, args.correlation)
     sc, dp, W, dW, pool = ts.sc, ts.dp, ts.W, ts.dW, ts.pool
     for q in range(args.warmup):
         ts.eager(q)
@@ -661,17 +722,19 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(t2, op=dist.ReduceOp.MAX)
     e2e_value = N * world / (float(t2[0]) / 1e3)
-    h2d = hA.numel() * 4 + hne.numel() * 4 + hdB.numel() * 4 + (hU.numel() * 4 if hU is not None else 0)
-    d2h = hdW.numel() * 4 * (2 if args.double_backward else 1)
+    esz = A.element_size()
+    h2d = hA.numel() * esz + hne.numel() * 4 + hdB.numel() * esz + (hU.numel() * esz if hU is not None else 0)
+    d2h = hdW.numel() * esz * (2 if args.double_backward else 1)
 
     if rank == 0:
         ops = alg_ops(sc)
         K = cfg.channels
         clocks = clk.summary()
         sm_mhz = clocks.get("sm_mhz") or 1965.0
-        peak_alu = 148 * 128 * sm_mhz * 1e6 / 1e12          # T lane-ops/s at the sampled clock
+        lanes, lanes_src = (fp64_lanes_per_sm_clk() if args.dtype == "f64" else (128.0, "148 SMs x 128 FP32 lanes"))
+        peak_alu = 148 * lanes * sm_mhz * 1e6 / 1e12          # T lane-ops/s at the sampled clock
         mean_nodes = nodes / args.steps
-        roof = kernel_roofline(args, cfg, sc, ops, prof, mean_nodes, peak_alu, sm_mhz)
+        roof = kernel_roofline(args, cfg, sc, ops, prof, mean_nodes, peak_alu, sm_mhz, esz, lanes, lanes_src)
         path_ops = (ops["path"] + (ops["bwd2"] + ops["bwd2_dW"] if args.double_backward else 0)) * mean_nodes * K
         kernels = {k: {"launches": v[0], "avg_ms": v[1] / max(v[0], 1)} for k, v in prof.items()}
         ms_step = ms_max / args.steps
@@ -691,7 +754,7 @@ def run_ours(args):
             "metric": "symcon_fwd_bwd_bwd2_nodes_per_s" if args.double_backward else "symcon_fwd_bwd_nodes_per_s",
             "value": value, "unit": "nodes/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": config,
             "per_gpu_nodes_per_s": value / world,
             "per_rank_ms_per_step": per_rank_ms,
@@ -699,7 +762,7 @@ def run_ours(args):
                              else {"note": "one molecule batch per rank (no Alg. 1 bins)"}),
             "path_tops": path_ops / (ms_step / 1e3) / 1e12,
             "path_frac_of_alu_peak": path_ops / (ms_step / 1e3) / 1e12 / peak_alu,
-            "path_roofline": path_roofline(cfg, sc, mean_nodes, path_ops, ms_step, args.double_backward, sm_mhz),
+            "path_roofline": path_roofline(cfg, sc, mean_nodes, path_ops, ms_step, args.double_backward, sm_mhz, esz, lanes),
             "roofline": roof, "kernels": kernels, "alg_ops_per_node_channel": ops,
             "step_breakdown_ms": {"step": ms_step, "kernels_back_to_back": ksum,
                                   "allreduce_alone": ar_ms,
@@ -720,7 +783,7 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def kernel_roofline(args, cfg, sc, ops, prof, mean_nodes, peak_alu, sm_mhz):
+def kernel_roofline(args, cfg, sc, ops, prof, mean_nodes, peak_alu, sm_mhz, esz=4, lanes=128.0, lanes_src=None):
     """roofline of the dominant kernel (by measured time): its algorithmic ops (or bytes) per launch
     / its average CUDA-event launch time, against the FP32 peak at the sampled SM clock (or the
     measured HBM copy bandwidth), whichever binds it."""
@@ -737,12 +800,13 @@ def kernel_roofline(args, cfg, sc, ops, prof, mean_nodes, peak_alu, sm_mhz):
     achieved = per_nc * mean_nodes * K / (avg_ms / 1e3) / 1e12   # T lane-ops/s
     nlm = (cfg.lmax_in + 1) ** 2
     outc = sc.out_dim // K
-    alg_b = {"symcon_fwd": 4 * (nlm + outc), "symcon_bwd_dA": 4 * (2 * nlm + outc),
-             "symcon_bwd_dW": 4 * (nlm + outc), "symcon_bwd2": 4 * (4 * nlm + 2 * outc),
-             "symcon_bwd2_dW": 4 * (2 * nlm + outc)}[kern] * mean_nodes * K
+    alg_b = {"symcon_fwd": esz * (nlm + outc), "symcon_bwd_dA": esz * (2 * nlm + outc),
+             "symcon_bwd_dW": esz * (nlm + outc), "symcon_bwd2": esz * (4 * nlm + 2 * outc),
+             "symcon_bwd2_dW": esz * (2 * nlm + outc)}[kern] * mean_nodes * K
     traffic, tsrc = None, None
     for tpath in (os.path.join(ROOT, "profiles", "r02", "ncu_traffic.json"),):
-        if os.path.exists(tpath) and args.config == "mp_medium" and args.capacity == DEFAULT_CAPACITY["mp_medium"]:
+        if (os.path.exists(tpath) and args.config == "mp_medium" and args.capacity == DEFAULT_CAPACITY["mp_medium"]
+                and args.dtype == "f32" and not args.correlation):
             tj = json.load(open(tpath))
             rec = tj["kernels"].get(kern)
             if rec:
@@ -759,11 +823,12 @@ def kernel_roofline(args, cfg, sc, ops, prof, mean_nodes, peak_alu, sm_mhz):
         return dict(common, bound="hbm", achieved=gbs, peak=hbm_peak, unit="GB/s", frac=gbs / hbm_peak,
                     alu_tops=achieved, alu_frac=achieved / peak_alu,
                     peak_derivation="MEASURED_PEAKS.json hbm_gbs (copy bandwidth)")
-    return dict(common, bound="alu", achieved=achieved, peak=peak_alu, unit="Tops/s (fp32 FMA lane-ops)",
+    prec = "fp64 DFMA" if esz == 8 else "fp32 FMA"
+    return dict(common, bound="alu", achieved=achieved, peak=peak_alu, unit=f"Tops/s ({prec} lane-ops)",
                 frac=achieved / peak_alu, hbm_gbs=alg_b / (avg_ms / 1e3) / 1e9,
-                frac_at_max_clock=achieved / (148 * 128 * 1.965e-3),
-                peak_derivation=f"148 SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (median SM clock sampled during the "
-                                "timed region; DESIGN.md §7)")
+                frac_at_max_clock=achieved / (148 * lanes * 1.965e-3),
+                peak_derivation=f"148 SMs x {lanes:g} lanes per clock ({lanes_src or 'FP32'}) x {sm_mhz:.0f} MHz (median SM "
+                                "clock sampled during the timed region; DESIGN.md §7)")
 
 
 # ----------------------------------------------------------------------------- channelwise TP
@@ -819,7 +884,8 @@ def run_tp(args):
             ev[1].record()
         _lib.symcon_tp_backward(tp.plan, x["N"], x["E"], x["Y"].data_ptr(), x["h"].data_ptr(), x["R"].data_ptr(),
                                 x["s"].data_ptr(), x["r"].data_ptr(), x["dA"].data_ptr(), x["dY"].data_ptr(),
-                                x["dh"].data_ptr(), x["dR"].data_ptr(), ws.data_ptr(), ws.numel(), st)
+                                x["dh"].data_ptr(), x["dR"].data_ptr(), ws.data_ptr(), ws.numel(), st,
+                                _lib.SYMCON_TP_REUSE_GRAPH)   # the step's graph, built by its forward
         launches[0] += tp.last_launch_count()
         if ev:
             ev[2].record()
@@ -886,7 +952,7 @@ def run_tp(args):
             dev_bufs[k].copy_(hsrc, non_blocking=True)
         tp.forward_raw(dev_bufs["Y"], dev_bufs["h"], dev_bufs["R"], dev_bufs["s"], dev_bufs["r"], A=x["A"])
         dY, dh, dR = tp.backward_raw(dev_bufs["Y"], dev_bufs["h"], dev_bufs["R"], dev_bufs["s"], dev_bufs["r"],
-                                     dev_bufs["dA"])
+                                     dev_bufs["dA"], reuse=True)
         hdY.copy_(dY, non_blocking=True)
         hdh.copy_(dh, non_blocking=True)
         hdR.copy_(dR, non_blocking=True)

@@ -305,6 +305,19 @@ symcon_status symcon_tp_backward(const symcon_tp_plan* plan, int64_t num_nodes, 
                                  const float* Y, const float* h, const float* R, const int32_t* sender,
                                  const int32_t* receiver, const float* dA, float* dY, float* dh, float* dR,
                                  void* ws, size_t ws_bytes, void* stream /* cudaStream_t */);
+/* The same with flags: SYMCON_TP_REUSE_GRAPH keeps the graph structure (the receiver-offset check and
+ * CSR, and the sender CSR of the backward) that the last TP call on `ws` built for the same sender /
+ * receiver pointers, N and E; the caller guarantees the index arrays are unchanged since that call
+ * (e.g. the backward of a step after its forward). Otherwise (or on any mismatch) it is rebuilt. */
+#define SYMCON_TP_REUSE_GRAPH 4u
+symcon_status symcon_tp_forward_ex(const symcon_tp_plan* plan, int64_t num_nodes, int64_t num_edges,
+                                   const float* Y, const float* h, const float* R, const int32_t* sender,
+                                   const int32_t* receiver, float* A, void* ws, size_t ws_bytes, uint32_t flags,
+                                   void* stream);
+symcon_status symcon_tp_backward_ex(const symcon_tp_plan* plan, int64_t num_nodes, int64_t num_edges,
+                                    const float* Y, const float* h, const float* R, const int32_t* sender,
+                                    const int32_t* receiver, const float* dA, float* dY, float* dh, float* dR,
+                                    void* ws, size_t ws_bytes, uint32_t flags, void* stream);
 /* Double backward of the TP (the derivatives of <(uY, uh, uR), (dY, dh, dR)(Y, h, R, dA)> and of <uA_bar...>:
  * the TP is linear in each of Y, h, R, so every term is a TP pass with one input replaced by its
  * cotangent, summed on the device (no caller arithmetic):
@@ -318,6 +331,13 @@ symcon_status symcon_tp_backward2(const symcon_tp_plan* plan, int64_t num_nodes,
                                   const int32_t* receiver, const float* dA, const float* uY, const float* uh,
                                   const float* uR, float* dA_bar, float* Y_bar, float* h_bar, float* R_bar,
                                   void* ws, size_t ws_bytes, void* stream /* cudaStream_t */);
+/* The same with flags (SYMCON_TP_REUSE_GRAPH for the first of its six passes; the other five always
+ * reuse the structure the first one built). */
+symcon_status symcon_tp_backward2_ex(const symcon_tp_plan* plan, int64_t num_nodes, int64_t num_edges,
+                                     const float* Y, const float* h, const float* R, const int32_t* sender,
+                                     const int32_t* receiver, const float* dA, const float* uY, const float* uh,
+                                     const float* uR, float* dA_bar, float* Y_bar, float* h_bar, float* R_bar,
+                                     void* ws, size_t ws_bytes, uint32_t flags, void* stream);
 /* Synchronises `stream`; SYMCON_EINVAL if the last TP call on `ws` saw unsorted receivers or an
  * out-of-range node index (*first_bad_edge = the first such edge), SYMCON_ECUDA on CUDA errors. */
 symcon_status symcon_tp_check_device_error(const symcon_tp_plan* plan, void* ws, void* stream,

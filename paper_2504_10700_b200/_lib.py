@@ -28,6 +28,7 @@ EXPORTS = ["symcon_build_tables", "symcon_plan_info", "symcon_plan_path", "symco
            "symcon_tp_last_launch_count", "symcon_tp_source", "symcon_tp_destroy", "symcon_peer_allreduce",
            "symcon_tp_precompile", "symcon_peer_allreduce_dev", "symcon_peer_allreduce_ex", "symcon_peer_check",
            "symcon_peer_allreduce_emulate", "symcon_backward2_ex", "symcon_tp_backward2", "symcon_tp_workspace2_bytes",
+           "symcon_tp_forward_ex", "symcon_tp_backward_ex", "symcon_tp_backward2_ex", "symcon_plan_sym_table4",
            "symcon_build_tables_ex", "symcon_forward_f64", "symcon_backward_f64", "symcon_precompile_ex"]
 SYMCON_F32, SYMCON_F64 = 0, 1
 
@@ -322,17 +323,28 @@ def symcon_tp_workspace2_bytes(plan, num_nodes, num_edges):
 
 
 def symcon_tp_backward2(plan, N, E, Y, h, R, sender, receiver, dA, uY, uh, uR, dA_bar, Y_bar, h_bar, R_bar, ws, ws_bytes,
-                        stream):
-    check(lib.symcon_tp_backward2(plan, N, E, Y, h, R, sender, receiver, dA, uY, uh, uR, dA_bar, Y_bar, h_bar, R_bar, ws,
-                                  ws_bytes, stream), "symcon_tp_backward2")
+                        stream, flags=0):
+    check(lib.symcon_tp_backward2_ex(plan, N, E, Y, h, R, sender, receiver, dA, uY, uh, uR, dA_bar, Y_bar, h_bar, R_bar, ws,
+                                     ws_bytes, flags, stream), "symcon_tp_backward2")
 
 
-def symcon_tp_forward(plan, N, E, Y, h, R, sender, receiver, A, ws, ws_bytes, stream):
-    check(lib.symcon_tp_forward(plan, N, E, Y, h, R, sender, receiver, A, ws, ws_bytes, stream), "symcon_tp_forward")
+SYMCON_TP_REUSE_GRAPH = 4
+lib.symcon_tp_forward_ex.argtypes = [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, ctypes.c_uint32, _vp]
+lib.symcon_tp_forward_ex.restype = ctypes.c_int
+lib.symcon_tp_backward_ex.argtypes = [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz,
+                                      ctypes.c_uint32, _vp]
+lib.symcon_tp_backward_ex.restype = ctypes.c_int
+lib.symcon_tp_backward2_ex.argtypes = [_vp, _i64, _i64] + [_vp] * 14 + [_sz, ctypes.c_uint32, _vp]
+lib.symcon_tp_backward2_ex.restype = ctypes.c_int
 
 
-def symcon_tp_backward(plan, N, E, Y, h, R, sender, receiver, dA, dY, dh, dR, ws, ws_bytes, stream):
-    check(lib.symcon_tp_backward(plan, N, E, Y, h, R, sender, receiver, dA, dY, dh, dR, ws, ws_bytes, stream),
+def symcon_tp_forward(plan, N, E, Y, h, R, sender, receiver, A, ws, ws_bytes, stream, flags=0):
+    check(lib.symcon_tp_forward_ex(plan, N, E, Y, h, R, sender, receiver, A, ws, ws_bytes, flags, stream),
+          "symcon_tp_forward")
+
+
+def symcon_tp_backward(plan, N, E, Y, h, R, sender, receiver, dA, dY, dh, dR, ws, ws_bytes, stream, flags=0):
+    check(lib.symcon_tp_backward_ex(plan, N, E, Y, h, R, sender, receiver, dA, dY, dh, dR, ws, ws_bytes, flags, stream),
           "symcon_tp_backward")
 
 

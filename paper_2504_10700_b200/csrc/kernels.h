@@ -57,6 +57,7 @@ struct TPCsrArgs {
   int* send_cur;            // [N]
   int* send_perm;           // [E]
   int* send_pos;            // [E] position of edge e in the sender CSR (inverse of send_perm)
+  int skip_recv;            // 1: the check and recv_off are already in the workspace (graph reuse)
 };
 int tp_csr_launch(const TPCsrArgs& a, cudaStream_t st);
 // dst[i] += src[i] for i < n (dst, src 16-byte aligned)

@@ -158,13 +158,15 @@ int grid_for(long long n, int threads) {
 
 int tp_csr_launch(const TPCsrArgs& a, cudaStream_t st) {
   int n = 0;
-  cudaMemsetAsync(a.err, 0xff, sizeof(unsigned long long), st);
-  if (a.E > 0) {
-    tp_check<<<grid_for(a.E, 256), 256, 0, st>>>(a.sender, a.receiver, a.N, a.E, a.err);
+  if (!a.skip_recv) {
+    cudaMemsetAsync(a.err, 0xff, sizeof(unsigned long long), st);
+    if (a.E > 0) {
+      tp_check<<<grid_for(a.E, 256), 256, 0, st>>>(a.sender, a.receiver, a.N, a.E, a.err);
+      n++;
+    }
+    tp_recv_off<<<grid_for(a.N + 1, 256), 256, 0, st>>>(a.receiver, a.N, a.E, a.recv_off);
     n++;
   }
-  tp_recv_off<<<grid_for(a.N + 1, 256), 256, 0, st>>>(a.receiver, a.N, a.E, a.recv_off);
-  n++;
   if (a.send_off) {
     cudaMemsetAsync(a.send_cnt, 0, sizeof(int) * (a.N > 0 ? a.N : 1), st);
     if (a.E > 0) { tp_send_hist<<<grid_for(a.E, 256), 256, 0, st>>>(a.sender, a.N, a.E, a.send_cnt); n++; }

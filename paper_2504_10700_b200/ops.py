@@ -236,7 +236,9 @@ class ChannelwiseTP:
                                ws.data_ptr(), ws.numel(), _stream_ptr(self.device))
         return A
 
-    def backward_raw(self, Y, h, R, sender, receiver, dA, need_Y=True, need_h=True, need_R=True):
+    def backward_raw(self, Y, h, R, sender, receiver, dA, need_Y=True, need_h=True, need_R=True, reuse=False):
+        """reuse=True: the sender / receiver arrays are those of the last call on this workspace, unchanged
+        since (SYMCON_TP_REUSE_GRAPH: the graph structure built then is kept)."""
         N, E = self._check(Y, h, R, sender, receiver)
         assert dA.dtype == torch.float32 and dA.is_contiguous() and dA.shape == (N, self.channels, self.n_out)
         dY = torch.empty_like(Y) if need_Y else None
@@ -245,7 +247,8 @@ class ChannelwiseTP:
         ws = self.workspace(N, E)
         ptr = lambda t: t.data_ptr() if (t is not None and t.numel()) else None
         _lib.symcon_tp_backward(self.plan, N, E, ptr(Y), ptr(h), ptr(R), ptr(sender), ptr(receiver), dA.data_ptr(),
-                                ptr(dY), ptr(dh), ptr(dR), ws.data_ptr(), ws.numel(), _stream_ptr(self.device))
+                                ptr(dY), ptr(dh), ptr(dR), ws.data_ptr(), ws.numel(), _stream_ptr(self.device),
+                                _lib.SYMCON_TP_REUSE_GRAPH if reuse else 0)
         return dY, dh, dR
 
     def backward2_raw(self, Y, h, R, sender, receiver, dA, uY, uh, uR):
@@ -290,7 +293,8 @@ class _TPFn(torch.autograd.Function):
             # create_graph=True (forces in the loss flow through Y and R): differentiable backward
             dY, dh, dR = _TPBwdFn.apply(Y, h, R, sender, receiver, dA.contiguous(), ctx.tp)
             return dY, dh, dR, None, None, None
-        dY, dh, dR = ctx.tp.backward_raw(Y, h, R, sender, receiver, dA.contiguous(), *ctx.needs_input_grad[:3])
+        # sender / receiver are saved tensors (autograd rejects in-place changes): keep the forward's graph structure
+        dY, dh, dR = ctx.tp.backward_raw(Y, h, R, sender, receiver, dA.contiguous(), *ctx.needs_input_grad[:3], reuse=True)
         return dY, dh, dR, None, None, None
 
 

@@ -44,3 +44,22 @@ def test_tp_bytes_and_path_roofline():
     r = bench.path_roofline(CONFIGS["mp_medium"], S(), 50_000, 3146 * 50_000 * 128, 1.2, False)
     assert r["bytes_per_node_channel"] == 224 and r["bound"] == "alu"
     assert abs(r["t_alu_ms"] - 3146 * 50_000 * 128 / (148 * 128 * 1.965e9) * 1e3) < 1e-9
+
+
+def test_alg_ops_trie_generalises_alg_ops(L):
+    """The prefix-trie counts (any degree; the correlation-4 bench lines) equal the degree-3 formulas
+    exactly at correlation 3, and at correlation 4 the forward count is the trie size."""
+    import bench
+
+    class _P:
+        pass
+    for corr, outs in [(3, (0,)), (3, (0, 1)), (3, (0, 1, 2)), (4, (0,))]:
+        s = _P()
+        s.plan, s.correlation = L.symcon_build_tables(3, corr, list(outs), 1, 1, -1), corr
+        t = bench.alg_ops_trie(s)
+        if corr == 3:
+            o = bench.alg_ops(s)
+            assert all(t[k] == o[k] for k in ("fwd", "dA", "dW", "path")), (outs, t, o)
+        else:
+            assert t["fwd"] == t["trie_nodes"] and t["path"] == t["fwd"] + t["dA"] + t["dW"]
+        L.symcon_destroy(s.plan)

@@ -195,3 +195,41 @@ def test_tp_double_backward_force_style_loss():
     _, ch, cR = backward(prob, u1, hh, hR, hs, hr, N, hRb)
     for got, ref in ((Yg.grad, aY + bY), (hg.grad, bh + ch), (Rg.grad, aR + cR), (Rbg.grad, dA_bar)):
         assert _rel(got.cpu(), ref) < TOL
+
+
+def test_tp_graph_reuse_flag():
+    """SYMCON_TP_REUSE_GRAPH (the backward of a step keeps the receiver / sender CSR its forward or an
+    earlier backward built on the same workspace): outputs bitwise equal to the rebuild path, fewer
+    launches; a different graph with the flag set (other pointers) is detected and rebuilt; the oracle
+    still agrees on the second graph."""
+    from oracle.tp import TPProblem, backward
+    tp, Y, h, R, s, r, N = _setup(3, (0, 1), 3, 64, [30, 22, 41], seed=4)
+    dA = torch.randn((N, 64, tp.n_out), generator=torch.Generator("cuda").manual_seed(2), device="cuda")
+    tp.forward_raw(Y, h, R, s, r)
+    ref = tp.backward_raw(Y, h, R, s, r, dA)                 # rebuilds everything
+    n_full = tp.last_launch_count()
+    tp.forward_raw(Y, h, R, s, r)
+    got = tp.backward_raw(Y, h, R, s, r, dA, reuse=True)     # recv part from the forward
+    n_reuse1 = tp.last_launch_count()
+    got2 = tp.backward_raw(Y, h, R, s, r, dA, reuse=True)    # recv and sender CSR both kept
+    n_reuse2 = tp.last_launch_count()
+    torch.cuda.synchronize()
+    assert tp.check_device_error()[0] == 0
+    for a, b, c in zip(ref, got, got2):
+        assert torch.equal(a, b) and torch.equal(a, c)
+    assert n_reuse2 < n_reuse1 < n_full, (n_full, n_reuse1, n_reuse2)
+    # another graph (new index tensors) with the flag: must not reuse the old structure
+    from synth.inputs import gen_tp_graph
+    sizes2 = [25, 47]
+    s2, r2 = gen_tp_graph(sizes2, 30, 9)
+    N2, E2 = int(sum(sizes2)), len(s2)
+    s2, r2 = torch.from_numpy(s2).cuda(), torch.from_numpy(r2).cuda()
+    Y2, h2, R2 = Y[:E2].contiguous(), h[:N2].contiguous(), R[:E2].contiguous()
+    dA2 = dA[:N2].contiguous()
+    dY2, dh2, dR2 = tp.backward_raw(Y2, h2, R2, s2, r2, dA2, reuse=True)
+    torch.cuda.synchronize()
+    assert tp.check_device_error()[0] == 0
+    prob = TPProblem(3, (0, 1), 3)
+    hY, hh, hR, hs, hr, hdA = _host(Y2, h2, R2, s2, r2, dA2)
+    rY, rh, rR = backward(prob, hY, hh, hR, hs, hr, N2, hdA)
+    assert _rel(dY2.cpu(), rY) < TOL and _rel(dh2.cpu(), rh) < TOL and _rel(dR2.cpu(), rR) < TOL
