@@ -58,7 +58,7 @@ def parse(argv=None):
     ap.add_argument("--allreduce", default="peer", choices=["peer", "nccl"],
                     help="N > 1: dW all-reduce by libsymcon's NVLink peer-memory kernel (default) or NCCL")
     ap.add_argument("--peer-algo", type=int, default=0, choices=[0, 1, 2],
-                    help="peer all-reduce: 0 auto (two-shot at N >= 4), 1 one-shot, 2 two-shot")
+                    help="peer all-reduce: 0 auto (two-shot at N >= 8), 1 one-shot, 2 two-shot")
     ap.add_argument("--sequential-bwd", action="store_true", help="run the dW and dA kernels back to back on one stream")
     ap.add_argument("--concurrent-bwd", action="store_true", help="run dA on a side stream concurrent with dW (default)")
     ap.add_argument("--channelwise-tp", action="store_true",

@@ -233,7 +233,7 @@ symcon_status symcon_pack_balanced(const int64_t* sizes, int64_t n, int64_t capa
  *   algo 2, two-shot: the same barrier; rank r sums slice r of all partials (rank order) in place
  *     into slice r of bufs[r]; a second barrier on slots [world, 2 world); out gathers slice q
  *     from bufs[q]. NVLink reads per rank: 2 (world-1)/world x n floats instead of (world-1) x n.
- *   algo 0: auto (two-shot for world >= 4).
+ *   algo 0: auto (two-shot for world >= 8; one-shot measured faster at 2 and 4 GPUs).
  * Every rank ends with bitwise the same out (each element summed once, in rank order).
  * The caller must not overwrite bufs[rank] until every rank's call has completed (alternate two
  * buffers per step); with algo 2, bufs[rank] is modified. out must not alias any bufs[r].

@@ -53,6 +53,11 @@ struct symcon_plan {
   int grid_dA_s = 0;
   size_t dw_r_smem = 0;
   mutable std::atomic<int> last_launches{0};
+  // the W-fold runs on this stream concurrently with the element bucketing (fork / join by events;
+  // works under stream capture)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  mutable std::mutex fork_mu;
   // optional launch timer (symcon_profile_*): CUDA events around each launch group
   struct Rec { int kind; cudaEvent_t a, b; };
   mutable std::mutex prof_mu;
@@ -168,13 +173,24 @@ size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 size_t esz(const symcon_plan* p) { return p->t.f64 ? sizeof(double) : sizeof(float); }
 
+// tiles per dW item for a call with N nodes: the plan's value, lowered for small N when the dW_r kernel
+// (one CTA per (item, 32-channel block), items processed serially) would otherwise be bound by its
+// longest item: at most N / (64 x the CTA slots per channel block) nodes per item (148 SMs x 3 CTAs)
+int tiles_per_item(const symcon_plan* p, int64_t N) {
+  const int t = p->kc.dw_tiles_per_item;
+  if (!p->kc.dw_r || p->t.simple) return t;
+  const int64_t slots = std::max<int64_t>(1, 148 * 3 / ((p->t.K + 31) / 32));
+  const int64_t want = N / ((int64_t)p->kc.tile_nodes * slots);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(t, want));
+}
+
 WsLayout layout(const symcon_plan* p, int64_t N) {
   WsLayout w{};
   const size_t fs = esz(p);
   const int E = p->t.E, K = p->t.K;
   const size_t nch = bucket_chunks(N);
   w.max_tiles = N / p->kc.tile_nodes + E + 1;
-  w.max_items = w.max_tiles / p->kc.dw_tiles_per_item + E + 1;
+  w.max_items = w.max_tiles / tiles_per_item(p, N) + E + 1;
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes); return r; };
   w.err = take(sizeof(unsigned long long));  // first: its offset must not depend on N
@@ -451,6 +467,11 @@ symcon_status symcon_build_tables_ex(int lmax_in, int correlation, const int* ou
     std::vector<char> cubin;
     if (!get_cubin(p->source, cubin, nullptr)) { cudaSetDevice(prev); delete p; return SYMCON_ECUDA; }
     s = cuda_err(cudaLibraryLoadData(&p->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0), "cudaLibraryLoadData");
+    if (!s && p->kc.fold_fork) {
+      s = cuda_err(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking), "aux stream");
+      if (!s) s = cuda_err(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming), "fork event");
+      if (!s) s = cuda_err(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming), "join event");
+    }
     if (!s && p->t.simple) {   // simple plan: fold, fwd, dA, dW, reduce_simple, unfold (codegen_simple.cpp)
       if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_fold, p->lib, "symcon_fold"), "get symcon_fold");
       if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_fwd, p->lib, "symcon_fwd"), "get symcon_fwd");
@@ -719,43 +740,57 @@ static int launch_prep(const symcon_plan* p, const WsLayout& w, char* ws, int64_
     if (fold) rec.W = W;
   }
   if (skip_fold) fold = false;
-  if (skip_bucket) goto after_bucket;
-  BucketArgs b;
-  b.node_elem = ne;
-  b.N = (int)N;
-  b.E = p->t.E;
-  b.tile_nodes = p->kc.tile_nodes;
-  b.tiles_per_item = p->kc.dw_tiles_per_item;
-  b.hist = (int*)(ws + w.hist);
-  b.off = (int*)(ws + w.off);
-  b.seg_off = (int*)(ws + w.seg_off);
-  b.perm = (int*)(ws + w.perm);
-  b.tiles = (int4*)(ws + w.tiles);
-  b.n_tiles = (int*)(ws + w.n_tiles);
-  b.items = (int4*)(ws + w.items);
-  b.n_items = (int*)(ws + w.n_items);
-  b.item_off = (int*)(ws + w.item_off);
-  b.err = (unsigned long long*)(ws + w.err);
-  b.tile_off = (int*)(ws + w.tile_off);
-  b.tile_perm = (int*)(ws + w.tile_perm);
-  b.max_tiles = w.max_tiles;
-  b.chunk_bad = (int*)(ws + w.chunk_bad);
-  b.zero_buf = (int*)(ws + w.dw_count);
-  b.zero_n = p->t.E * ((p->t.K + 31) / 32);
-  b.fused = p->kc.bucket_fused;
-  {
-    Timed tm(p, K_BUCKET, st);
-    n += bucket_launch(b, st);
-  }
-after_bucket:
-  if (fold) {
-    Timed tm(p, K_FOLD, st);
+  // the fold (W only) and the bucketing (node_elem only) are independent: fold on the plan's aux stream
+  std::unique_lock<std::mutex> fork_lock(p->fork_mu, std::defer_lock);
+  const bool fork = fold && !skip_bucket && p->aux;
+  auto launch_fold = [&](cudaStream_t fs) {
+    Timed tm(p, K_FOLD, fs);
     q.W = W;
     void* args[] = {&q};
     dim3 grid(p->t.E, (p->t.K + 31) / 32, p->kc.fold_split);
-    *s = cuda_err(cudaLaunchKernel((const void*)p->k_fold, grid, dim3(128), args, 0, st), "launch symcon_fold");
+    *s = cuda_err(cudaLaunchKernel((const void*)p->k_fold, grid, dim3(128), args, 0, fs), "launch symcon_fold");
     n++;
+  };
+  if (fork) {
+    fork_lock.lock();
+    cudaEventRecord(p->ev_fork, st);
+    cudaStreamWaitEvent(p->aux, p->ev_fork, 0);
+    launch_fold(p->aux);
+    cudaEventRecord(p->ev_join, p->aux);
+    fold = false;
   }
+  if (!skip_bucket) {
+    BucketArgs b;
+    b.node_elem = ne;
+    b.N = (int)N;
+    b.E = p->t.E;
+    b.tile_nodes = p->kc.tile_nodes;
+    b.tiles_per_item = tiles_per_item(p, N);
+    b.hist = (int*)(ws + w.hist);
+    b.off = (int*)(ws + w.off);
+    b.seg_off = (int*)(ws + w.seg_off);
+    b.perm = (int*)(ws + w.perm);
+    b.tiles = (int4*)(ws + w.tiles);
+    b.n_tiles = (int*)(ws + w.n_tiles);
+    b.items = (int4*)(ws + w.items);
+    b.n_items = (int*)(ws + w.n_items);
+    b.item_off = (int*)(ws + w.item_off);
+    b.err = (unsigned long long*)(ws + w.err);
+    b.tile_off = (int*)(ws + w.tile_off);
+    b.tile_perm = (int*)(ws + w.tile_perm);
+    b.max_tiles = w.max_tiles;
+    b.chunk_bad = (int*)(ws + w.chunk_bad);
+    b.zero_buf = (int*)(ws + w.dw_count);
+    b.zero_n = p->t.E * ((p->t.K + 31) / 32);
+    b.fused = p->kc.bucket_fused;
+    Timed tm(p, K_BUCKET, st);
+    n += bucket_launch(b, st);
+  }
+  if (fork) {
+    cudaStreamWaitEvent(st, p->ev_join, 0);
+    fork_lock.unlock();
+  }
+  if (fold) launch_fold(st);
   return n;
 }
 
@@ -1064,7 +1099,7 @@ symcon_status symcon_peer_allreduce_ex(const float* const* bufs, uint32_t* const
                                        int64_t spin_limit, float* out, int32_t* err, void* stream) {
   if (algo < 0 || algo > 2) { set_error("algo must be 0 (auto), 1 (one-shot) or 2 (two-shot)"); return SYMCON_EINVAL; }
   if (spin_limit < 0) { set_error("spin_limit must be >= 0"); return SYMCON_EINVAL; }
-  if (algo == 0) algo = world >= 4 ? 2 : 1;
+  if (algo == 0) algo = world >= 8 ? 2 : 1;   // measured: one-shot faster at 2 and 4
   return peer_common(bufs, pads, world, rank, n, epoch, epoch_counter, algo, spin_limit, out, err, stream);
 }
 
@@ -1192,6 +1227,9 @@ void symcon_destroy(symcon_plan* p) {
     for (auto& r : p->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : p->event_pool) cudaEventDestroy(e);
   }
+  if (p->aux) cudaStreamDestroy(p->aux);
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  if (p->ev_join) cudaEventDestroy(p->ev_join);
   if (p->lib) cudaLibraryUnload(p->lib);
   delete p;
 }

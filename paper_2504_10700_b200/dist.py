@@ -50,7 +50,7 @@ class BinPackedShards:
 
 class PeerReducer:
     """Two symmetric (peer-mapped) fp32 buffers used alternately per step + one signal pad; the
-    all-reduce itself is libsymcon's kernel (no NCCL). algo: 0 auto (two-shot for world >= 4),
+    all-reduce itself is libsymcon's kernel (no NCCL). algo: 0 auto (two-shot for world >= 8),
     1 one-shot, 2 two-shot (symcon_peer_allreduce_ex). A barrier timeout is a hard error: the
     kernel writes NaN and sets `err`; `check()` raises it (SYMCON_ETIMEOUT)."""
 

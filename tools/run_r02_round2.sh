@@ -7,7 +7,7 @@ nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/probes/dfma_probe tool
   timeout 120 tools/probes/dfma_probe > gpurun_out/r02b/dfma_probe.jsonl 2>&1; echo dfma_rc=$?
 mkdir -p profiles/r02 && cp gpurun_out/r02b/dfma_probe.jsonl profiles/r02/dfma_probe.jsonl
 timeout 600 python bench.py --steps 10 --warmup 3 --dtype f64 --cpu-sample 8192 > gpurun_out/r02b/bench_f64.json 2> gpurun_out/r02b/bench_f64.err; echo f64_rc=$?
-timeout 900 python bench.py --steps 10 --warmup 3 --correlation 4 --cpu-sample 4096 > gpurun_out/r02b/bench_corr4.json 2> gpurun_out/r02b/bench_corr4.err; echo c4_rc=$?
+timeout 900 python bench.py --steps 10 --warmup 3 --correlation 4 --cpu-sample 1024 > gpurun_out/r02b/bench_corr4.json 2> gpurun_out/r02b/bench_corr4.err; echo c4_rc=$?
 timeout 600 python bench.py --steps 20 --warmup 5 --double-backward --no-cpu-baseline > gpurun_out/r02b/bench_dbl_minb10.json 2> gpurun_out/r02b/bench_dbl_minb10.err; echo dbl10_rc=$?
 SYMCON_KCONFIG=bwd2_min_blocks=8 timeout 900 python bench.py --steps 20 --warmup 5 --double-backward --no-cpu-baseline > gpurun_out/r02b/bench_dbl_minb8.json 2> gpurun_out/r02b/bench_dbl_minb8.err; echo dbl8_rc=$?
 timeout 600 python bench.py --steps 20 --warmup 5 --channelwise-tp --no-cpu-baseline > gpurun_out/r02b/bench_tp.json 2> gpurun_out/r02b/bench_tp.err; echo tp_rc=$?
