@@ -178,7 +178,7 @@ size_t esz(const symcon_plan* p) { return p->t.f64 ? sizeof(double) : sizeof(flo
 // longest item: at most N / (64 x the CTA slots per channel block) nodes per item (148 SMs x 3 CTAs)
 int tiles_per_item(const symcon_plan* p, int64_t N) {
   const int t = p->kc.dw_tiles_per_item;
-  if (!p->kc.dw_r || p->t.simple) return t;
+  if (!p->kc.dw_r || p->t.simple || !p->kc.dw_items_adapt) return t;
   const int64_t slots = std::max<int64_t>(1, 148 * 3 / ((p->t.K + 31) / 32));
   const int64_t want = N / ((int64_t)p->kc.tile_nodes * slots);
   return (int)std::max<int64_t>(1, std::min<int64_t>(t, want));

@@ -104,6 +104,7 @@ struct KernelConfig {
   int simple_warps = 4;      // simple plans (fp64 / corr 4): warps per fwd / dA CTA (coefficient rows in dynamic smem)
   int simple_unfold_split = 1;  // simple plans: column split of the unfold grid (grid.z)
   int fold_fork = 1;         // run the W-fold on an auxiliary stream concurrently with the bucketing
+  int dw_items_adapt = 1;    // lower the tiles per dW item for small N (dW_r plans; api.cpp tiles_per_item)
 };
 std::string generate_source(const Tables& t, const KernelConfig& kc);
 // codegen_simple.cpp: plain scalar kernels of any degree (prefix-trie forward, reverse-mode dA), fp32 or fp64

@@ -1,4 +1,4 @@
-"""Write profiles/<round>/ artifacts from a tools/run_profile_round.sh capture.
+"""Write profiles/<round>/ artifacts from a tools/gpu/profile_round.sh capture.
 
     python tools/make_profile_artifacts.py r01c profiles/r01
 """
