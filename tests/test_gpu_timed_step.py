@@ -100,3 +100,35 @@ def test_timed_step_small_capacity_all_nodes():
         dAref, dWref = oc.backward(hA, hW, hne, hdB)
         Bq, dAq, dWq = snaps[q]
         assert _rel(Bq, Bref) < TOL and _rel(dAq, dAref) < TOL and _rel(dWq, dWref) < TOL, q
+
+
+@pytest.mark.parametrize("dtype,correlation,tol", [("f64", None, 1e-10), ("f32", 4, 1e-5)])
+def test_timed_step_variants_full_size_sampled(dtype, correlation, tol):
+    """The bench's timed step for the §8(f) row-3 variants at the full MP-medium size (bench.py
+    --dtype f64 / --correlation 4; C = 50,000, the same pool, streams and CUDA graphs): B and dA on
+    64 sampled nodes of one bin, dW on the four smallest elements present (all their nodes) and, in
+    fp64, on the Zipf-head element too (~10k nodes), against the C oracle."""
+    import bench
+    ts = bench.TimedStep(pool=2, dtype=dtype, correlation=correlation)
+    for q in range(2):
+        ts.eager(q)
+    torch.cuda.synchronize()
+    ts.capture()
+    snaps = _replay_and_snapshot(ts, cycles=1)
+    oc = _oracle(ts.cfg)
+    hW = ts.W.cpu().double().numpy()
+    b, N, A, ne, dB, B, dA = ts.pool[0]
+    hA, hne, hdB = A.cpu().double().numpy(), ne.cpu().numpy(), dB.cpu().double().numpy()
+    Bq, dAq, dWq = snaps[0]
+    idx = np.sort(np.random.default_rng(11).choice(N, 64, replace=False))
+    assert _rel(Bq[idx], oc.forward(hA[idx], hW, hne[idx])) < tol
+    assert _rel(dAq[idx], oc.backward(hA[idx], hW, hne[idx], hdB[idx], want_dW=False)[0]) < tol
+    counts = np.bincount(hne, minlength=hW.shape[0])
+    present = np.nonzero(counts)[0]
+    chosen = list(present[np.argsort(counts[present], kind="stable")[:4]])
+    if dtype == "f64":
+        chosen.append(int(np.argmax(counts)))
+    for z in chosen:
+        sel = np.nonzero(hne == z)[0]
+        _, dWref = oc.backward(hA[sel], hW, hne[sel], hdB[sel], want_dA=False)
+        assert _rel(dWq[z], dWref[z]) < tol, (dtype, correlation, z, counts[z])
