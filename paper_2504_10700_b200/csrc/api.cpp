@@ -425,14 +425,7 @@ static symcon_status build_common(int lmax_in, int corr, const int* out_L, int n
     while (p->kc.simple_warps > 1 && row_bytes * p->kc.simple_warps > 200 * 1024) p->kc.simple_warps--;
     if (row_bytes > 200 * 1024) { set_error("folded table too large for shared memory"); delete p; return SYMCON_EUNSUPPORTED; }
     p->simple_smem = row_bytes * p->kc.simple_warps;
-    // dW: RPG register accumulators per warp, at most 8 warps (row groups) per CTA, passes over the
-    // item's nodes if there are more groups (correlation 4)
-    p->kc.simple_dw_rpg = p->t.f64 ? 32 : 64;
-    {
-      const int ng = ((int)p->t.rows.size() + p->kc.simple_dw_rpg - 1) / p->kc.simple_dw_rpg;
-      const int npass = (ng + 7) / 8;
-      p->kc.simple_dw_warps = (ng + npass - 1) / npass;
-    }
+
     p->kc.unfold_reduce = 0;
     p->source = generate_source_simple(p->t, p->kc);
   } else {
@@ -937,8 +930,9 @@ static symcon_status backward_impl(const symcon_plan* p, int64_t N, const float*
   if (dW && p->t.simple) {   // simple plans: S partials (item, row group, channel block), item reduction, unfold
     {
       Timed tm(p, K_DW, st);
-      s = cuda_err(cudaLaunchKernel((const void*)p->k_dW, dim3((unsigned)w.max_items, (p->t.K + 31) / 32), dim3(32 * p->kc.simple_dw_warps),
-                                    args, 0, st), "launch symcon_bwd_dW (simple)");
+      const int ng = ((int)p->t.rows.size() + 47) / 48;   // = codegen_simple RPG 48
+      s = cuda_err(cudaLaunchKernel((const void*)p->k_dW, dim3((unsigned)w.max_items, ng, (p->t.K + 31) / 32), dim3(32), args, 0, st),
+                   "launch symcon_bwd_dW (simple)");
     }
     if (s) return s;
     Timed tm(p, K_UNFOLD, st);

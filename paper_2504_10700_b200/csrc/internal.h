@@ -103,8 +103,7 @@ struct KernelConfig {
   int da_s_minb = 0;         // da_s: __launch_bounds__ min blocks
   int simple_warps = 4;      // simple plans (fp64 / corr 4): warps per fwd / dA CTA (coefficient rows in dynamic smem)
   int simple_unfold_split = 1;  // simple plans: column split of the unfold grid (grid.z)
-  int simple_dw_rpg = 32;    // simple plans: dW rows per warp (register accumulators)
-  int simple_dw_warps = 8;   // simple plans: dW warps per CTA (row groups sharing the staged nodes)
+  int fwd_r_chains = 1;      // fwd_r: 2 splits the Horner T / B accumulation chains into even / odd halves
   int fold_fork = 1;         // run the W-fold on an auxiliary stream concurrently with the bucketing
   int dw_items_adapt = 1;    // lower the tiles per dW item for small N (dW_r plans; api.cpp tiles_per_item)
 };
