@@ -209,10 +209,10 @@ WsLayout layout(const symcon_plan* p, int64_t N) {
   w.coef = take(fs * (size_t)E * K * p->npad);
   w.spart = take(fs * (size_t)w.max_items * K * p->npad);
   w.stot = take(fs * (size_t)E * K * p->npad);
-  w.coef_r = take(sizeof(float) * (size_t)E * p->t.out_per_ch * std::max(p->rnq, 1) * K * 4);
+  w.coef_r = take(sizeof(float) * (size_t)E * p->t.out_per_ch * p->kc.fwd_r_split * std::max(p->rnq, 1) * K * 4);
   w.dw_count = take(sizeof(int) * (size_t)E * ((K + 31) / 32));
   w.coef2 = take(sizeof(float) * (size_t)E * K * p->npad);   // the uW fold of the double backward
-  w.coef_r2 = take(sizeof(float) * (size_t)E * p->t.out_per_ch * std::max(p->rnq, 1) * K * 4);
+  w.coef_r2 = take(sizeof(float) * (size_t)E * p->t.out_per_ch * p->kc.fwd_r_split * std::max(p->rnq, 1) * K * 4);
   w.total = o;
   return w;
 }
@@ -403,7 +403,8 @@ static symcon_status build_common(int lmax_in, int corr, const int* out_L, int n
     return SYMCON_EINVAL;
   }
   if (p->kc.fwd_r && !p->t.simple) {
-    for (auto& h : horner_slots(p->t)) p->rnq = std::max(p->rnq, (int)((h.rows.size() + 3) / 4));
+    if (p->kc.fwd_r_split != 1 && (p->kc.fwd_r_split != 2 || p->kc.fwd_r_npw != 1)) { set_error("fwd_r_split must be 1 or 2 (with fwd_r_npw 1)"); delete p; return SYMCON_EINVAL; }
+    for (auto& h : horner_vslots(p->t, p->kc.fwd_r_split)) p->rnq = std::max(p->rnq, (int)((h.rows.size() + 3) / 4));
     if (p->t.n_lm != 16) p->kc.fwd_r = 0;   // the A staging is laid out for 16 floats per (node, channel) (lmax_in 3)
   }
   // measured (profiles/r02): dW_r -22% at MP-medium (4 slots); slower with 1 slot (OFF) and 9 (large)
@@ -510,12 +511,14 @@ symcon_status symcon_build_tables_ex(int lmax_in, int correlation, const int* ou
       p->fwd_r_smem = sizeof(float) * p->kc.fwd_r_nst * (size_t)p->kc.fwd_r_block * 512 + 16 * p->kc.fwd_r_nst +
                       sizeof(int) * p->kc.fwd_r_nst * (size_t)p->kc.fwd_r_block;
       if (p->kc.fwd_r_tr) p->fwd_r_smem += sizeof(float) * (size_t)p->kc.fwd_r_block * 512 + 64;   // the interleaved copy
+      if (p->kc.fwd_r_split > 1) p->fwd_r_smem += 8 + sizeof(unsigned long long) * 2 * p->t.out_per_ch * 32;   // half-slot partials
       if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_fwd_r, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                            (int)p->fwd_r_smem, device), "fwd_r smem attribute");
       int sms = 0, occ = 0;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-      if (!s) s = cuda_err(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)p->k_fwd_r, 32 * p->t.out_per_ch,
-                                                                         p->fwd_r_smem), "occupancy fwd_r");
+      if (!s) s = cuda_err(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)p->k_fwd_r,
+                                                                         32 * p->t.out_per_ch * p->kc.fwd_r_split, p->fwd_r_smem),
+                           "occupancy fwd_r");
       if (p->kc.fwd_r_ctas_per_sm > 0) occ = std::min(occ, p->kc.fwd_r_ctas_per_sm);
       p->grid_fwd_r = sms * std::max(occ, 1);
     }
@@ -808,7 +811,8 @@ static symcon_status launch_fwd_kernel(const symcon_plan* p, const WsLayout& w, 
   void* args[] = {&q};
   Timed tm(p, K_FWD, st);
   if (p->k_fwd_r)
-    return cuda_err(cudaLaunchKernel((const void*)p->k_fwd_r, dim3(p->grid_fwd_r), dim3(32 * p->t.out_per_ch), args, p->fwd_r_smem, st),
+    return cuda_err(cudaLaunchKernel((const void*)p->k_fwd_r, dim3(p->grid_fwd_r), dim3(32 * p->t.out_per_ch * p->kc.fwd_r_split), args,
+                                     p->fwd_r_smem, st),
                     "launch symcon_fwd_r");
   if (p->k_fwd_g)
     return cuda_err(cudaLaunchKernel((const void*)p->k_fwd_g, dim3((unsigned)((w.max_tiles + 3) / 4), (p->t.K + 31) / 32), dim3(128),

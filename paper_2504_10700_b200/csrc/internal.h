@@ -103,6 +103,7 @@ struct KernelConfig {
   int da_s_minb = 0;         // da_s: __launch_bounds__ min blocks
   int simple_warps = 4;      // simple plans (fp64 / corr 4): warps per fwd / dA CTA (coefficient rows in dynamic smem)
   int simple_unfold_split = 1;  // simple plans: column split of the unfold grid (grid.z)
+  int fwd_r_split = 1;       // fwd_r: 2 = two warps per output slot (each half of the first indices), partial B summed in smem
   int fwd_r_chains = 1;      // fwd_r: 2 splits the Horner T / B accumulation chains into even / odd halves
   int fold_fork = 1;         // run the W-fold on an auxiliary stream concurrently with the bucketing
   int dw_items_adapt = 1;    // lower the tiles per dW item for small N (dW_r plans; api.cpp tiles_per_item)
@@ -114,8 +115,11 @@ std::string generate_source_simple(const Tables& t, const KernelConfig& kc);
 // Horner program of one output slot (symcon_fwd_r)
 struct HornerB { int b, row_ab; std::vector<std::pair<int, int>> cs; };   // (c, row j) of degree-3 rows
 struct HornerA { int a, row_a; std::vector<HornerB> bs; };
-struct HornerSlot { int slot; std::vector<HornerA> as; std::vector<int> rows; };  // rows: register order
+struct HornerSlot { int slot; std::vector<HornerA> as; std::vector<int> rows; int half = 0; };  // rows: register order
 std::vector<HornerSlot> horner_slots(const Tables& t);
+// fwd_r warps: the slots, or (fwd_r_split = 2) each slot's first indices split in two op-balanced halves
+// (slot-major: [s0 h0, s0 h1, s1 h0, ...]); the coefficient table coef_r is laid out per entry
+std::vector<HornerSlot> horner_vslots(const Tables& t, int split);
 int64_t horner_ops(const Tables& t);
 std::string generate_fwd_r(const Tables& t, const KernelConfig& kc);
 std::string generate_dw_r(const Tables& t, const KernelConfig& kc);
