@@ -1,6 +1,6 @@
-# bench.py (N=1, default workload) under several SYMCON_KCONFIG variants; one JSON line each
+# bench.py (N=1, default workload + $BENCH_ARGS) under several SYMCON_KCONFIG variants; one JSON line each
 for v in "$@"; do
-  SYMCON_KCONFIG="$v" timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bkc.json 2> gpurun_out/bkc.err
+  SYMCON_KCONFIG="$v" timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline $BENCH_ARGS > gpurun_out/bkc.json 2> gpurun_out/bkc.err
   python - "$v" <<'PY'
 import json, sys
 try:
