@@ -285,8 +285,11 @@ def path_roofline(cfg, sc, mean_nodes, path_ops, ms_step, dbl, sm_mhz=1965.0, es
     t_alu = path_ops / (148 * lanes * sm_mhz * 1e6)
     t_hbm = per * mean_nodes * K / (hbm * 1e9)
     bound = "alu" if t_alu >= t_hbm else "hbm"
-    return {"bound": bound, "frac": max(t_alu, t_hbm) / (ms_step / 1e3), "t_alu_ms": t_alu * 1e3, "t_hbm_ms": t_hbm * 1e3,
-            "bytes_per_node_channel": per, "sm_mhz": sm_mhz}
+    out = {"bound": bound, "frac": max(t_alu, t_hbm) / (ms_step / 1e3), "t_alu_ms": t_alu * 1e3, "t_hbm_ms": t_hbm * 1e3,
+           "bytes_per_node_channel": per, "sm_mhz": sm_mhz}
+    if bound == "hbm":   # also against the spec HBM bandwidth (8 TB/s)
+        out["frac_at_spec_hbm_8tbs"] = max(t_alu, per * mean_nodes * K / 8e12) / (ms_step / 1e3)
+    return out
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -620,7 +623,8 @@ def run_ours(args):
     pool_bytes = sum(x[2].nbytes + x[3].nbytes + x[4].nbytes + x[5].nbytes + x[6].nbytes for x in pool)
     flush = not (step_in > L2_BYTES or pool_bytes > 3 * L2_BYTES)
     scratch = torch.empty(int(2 * L2_BYTES), dtype=torch.uint8, device=dev) if flush else None
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)] if flush else None
+    # per-step event pairs (median / min per step beside the mean the line's value uses)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         # ranks enter the timed region together (the sampler start-up takes a variable fraction
         # of a second per rank; without this barrier the first rank's wait is charged to the others)
@@ -632,17 +636,17 @@ def run_ours(args):
         for q in range(args.steps):
             if flush:
                 scratch.zero_()
-                evs[q][0].record()
+            evs[q][0].record()
             nodes += ts.step(q)
-            if flush:
-                evs[q][1].record()
+            evs[q][1].record()
         e1.record()
         torch.cuda.synchronize()
         clk.end()
     if world > 1:
         dist.barrier()
     dp.check()
-    ms = sum(a.elapsed_time(b) for a, b in evs) if flush else e0.elapsed_time(e1)
+    step_ms = sorted(a.elapsed_time(b) for a, b in evs)
+    ms = sum(step_ms) if flush else e0.elapsed_time(e1)
     l2_note = (f"L2 flushed before every timed step (256 MB memset outside the step's CUDA-event pair; pool of "
                f"{len(pool)} bins = {pool_bytes / 1e6:.0f} MB, step inputs {step_in / 1e6:.0f} MB)" if flush else
                f"no flush: step inputs {step_in / 1e6:.0f} MB (A, node_elem, dB) and a pool of {len(pool)} distinct bins "
@@ -774,6 +778,8 @@ def run_ours(args):
             "config": config,
             "per_gpu_nodes_per_s": value / world,
             "per_rank_ms_per_step": per_rank_ms,
+            "step_ms_rank0": {"median": statistics.median(step_ms), "min": step_ms[0], "max": step_ms[-1],
+                              "note": "per-step CUDA-event pairs on rank 0 (the value uses the whole timed region)"},
             "edge_balance": (edge_spread(ts.sizes, ts.shards.offsets, ts.shards.ids, world, POOL) if ts.shards is not None
                              else {"note": "one molecule batch per rank (no Alg. 1 bins)"}),
             "path_tops": path_ops / (ms_step / 1e3) / 1e12,
