@@ -207,7 +207,7 @@ WsLayout layout(const symcon_plan* p, int64_t N) {
   w.tile_off = take(sizeof(int) * (E + 2));
   w.tile_perm = take(sizeof(int) * (size_t)w.max_tiles * p->kc.tile_nodes);
   w.coef = take(fs * (size_t)E * K * p->npad);
-  w.spart = take(fs * (size_t)w.max_items * K * p->npad);
+  w.spart = take(fs * (size_t)w.max_items * K * p->npad * (p->kc.dw_r ? p->kc.dw_r_wps : 1));   // dw_r_wps partials per item
   w.stot = take(fs * (size_t)E * K * p->npad);
   w.coef_r = take(sizeof(float) * (size_t)E * p->t.out_per_ch * p->kc.fwd_r_split * std::max(p->rnq, 1) * K * 4);
   w.dw_count = take(sizeof(int) * (size_t)E * ((K + 31) / 32));
@@ -404,6 +404,11 @@ static symcon_status build_common(int lmax_in, int corr, const int* out_L, int n
   }
   if (p->kc.fwd_r && !p->t.simple) {
     if (p->kc.fwd_r_split != 1 && (p->kc.fwd_r_split != 2 || p->kc.fwd_r_npw != 1)) { set_error("fwd_r_split must be 1 or 2 (with fwd_r_npw 1)"); delete p; return SYMCON_EINVAL; }
+    // measured (profiles/r02): with one output slot (OFF-small) a 1-warp CTA leaves 3 warps per SM;
+    // 4 warps sharing each stage's node pairs cut the forward 0.051 -> 0.036 ms
+    if (p->kc.fwd_r_wps <= 0) p->kc.fwd_r_wps = p->t.out_per_ch == 1 ? 4 : 1;
+    if (p->kc.fwd_r_split > 1) p->kc.fwd_r_wps = 1;
+    if (p->kc.fwd_r_wps < 1 || p->kc.fwd_r_wps * p->kc.fwd_r_npw > p->kc.fwd_r_block / 2) { set_error("bad fwd_r_wps"); delete p; return SYMCON_EINVAL; }
     for (auto& h : horner_vslots(p->t, p->kc.fwd_r_split)) p->rnq = std::max(p->rnq, (int)((h.rows.size() + 3) / 4));
     if (p->t.n_lm != 16) p->kc.fwd_r = 0;   // the A staging is laid out for 16 floats per (node, channel) (lmax_in 3)
   }
@@ -414,6 +419,12 @@ static symcon_status build_common(int lmax_in, int corr, const int* out_L, int n
   if (p->t.n_lm != 16) p->kc.dw_r = 0;
   if (p->kc.da_s < 0) p->kc.da_s = 0;
   if (p->kc.dw_r_block < 2 || 64 % p->kc.dw_r_block) { set_error("bad dw_r_block"); delete p; return SYMCON_EINVAL; }
+  // dW_r warps per slot: auto 4 with one output slot (a 1-warp CTA leaves too few warps per SM), else 1;
+  // at most 16 warps per CTA
+  if (p->kc.dw_r_wps <= 0) p->kc.dw_r_wps = p->t.out_per_ch == 1 ? 4 : 1;
+  if (32 * p->t.out_per_ch * std::max(1, p->kc.dw_r_split) * p->kc.dw_r_wps > 512) p->kc.dw_r_wps = 1;
+  if (p->kc.dw_r_wps > p->kc.dw_r_block) { set_error("bad dw_r_wps"); delete p; return SYMCON_EINVAL; }
+  if (p->kc.dw_r_wps > 1) { p->kc.unfold_reduce = 0; p->kc.dw_r_fuse = 0; }
   if (p->t.simple) {   // fp64 or correlation 4: the plain scalar kernels of codegen_simple.cpp
     p->kc.fwd_r = p->kc.dw_r = p->kc.da_s = 0;
     p->kc.gamma = 0;
@@ -517,8 +528,8 @@ symcon_status symcon_build_tables_ex(int lmax_in, int correlation, const int* ou
       int sms = 0, occ = 0;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
       if (!s) s = cuda_err(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)p->k_fwd_r,
-                                                                         32 * p->t.out_per_ch * p->kc.fwd_r_split, p->fwd_r_smem),
-                           "occupancy fwd_r");
+                                                                         32 * p->t.out_per_ch * p->kc.fwd_r_split * p->kc.fwd_r_wps,
+                                                                         p->fwd_r_smem), "occupancy fwd_r");
       if (p->kc.fwd_r_ctas_per_sm > 0) occ = std::min(occ, p->kc.fwd_r_ctas_per_sm);
       p->grid_fwd_r = sms * std::max(occ, 1);
     }
@@ -811,8 +822,8 @@ static symcon_status launch_fwd_kernel(const symcon_plan* p, const WsLayout& w, 
   void* args[] = {&q};
   Timed tm(p, K_FWD, st);
   if (p->k_fwd_r)
-    return cuda_err(cudaLaunchKernel((const void*)p->k_fwd_r, dim3(p->grid_fwd_r), dim3(32 * p->t.out_per_ch * p->kc.fwd_r_split), args,
-                                     p->fwd_r_smem, st),
+    return cuda_err(cudaLaunchKernel((const void*)p->k_fwd_r, dim3(p->grid_fwd_r),
+                                     dim3(32 * p->t.out_per_ch * p->kc.fwd_r_split * p->kc.fwd_r_wps), args, p->fwd_r_smem, st),
                     "launch symcon_fwd_r");
   if (p->k_fwd_g)
     return cuda_err(cudaLaunchKernel((const void*)p->k_fwd_g, dim3((unsigned)((w.max_tiles + 3) / 4), (p->t.K + 31) / 32), dim3(128),
@@ -953,7 +964,7 @@ static symcon_status backward_impl(const symcon_plan* p, int64_t N, const float*
     Timed tm(p, K_DW, st);
     if (p->k_dW_r)   // S partials (+ with dw_r_fuse the element's item reduction and the unfold)
       s = cuda_err(cudaLaunchKernel((const void*)p->k_dW_r, dim3((unsigned)(w.max_items + (p->kc.dw_r_fuse ? p->t.E : 0)), p->t.K / 32, 1),
-                                    dim3(32 * p->t.out_per_ch * std::max(1, p->kc.dw_r_split)), args, p->dw_r_smem, st),
+                                    dim3(32 * p->t.out_per_ch * std::max(1, p->kc.dw_r_split) * p->kc.dw_r_wps), args, p->dw_r_smem, st),
                    "launch symcon_bwd_dW_r");
     else
       s = cuda_err(cudaLaunchKernel((const void*)p->k_dW, dim3((unsigned)(w.max_items * p->dw_nz), (p->t.K + 31) / 32, 1),
@@ -962,7 +973,8 @@ static symcon_status backward_impl(const symcon_plan* p, int64_t N, const float*
     if (s) return s;
     if (!p->k_dW_r || !p->kc.dw_r_fuse) {
       Timed tm(p, K_UNFOLD, st);
-      if (!p->kc.unfold_reduce) n += reduce_items_launch(q.spart, q.item_off, p->t.E, p->npad, p->t.K, q.stot, st);
+      if (!p->kc.unfold_reduce)
+        n += reduce_items_launch(q.spart, q.item_off, p->t.E, p->npad, p->t.K, q.stot, st, p->k_dW_r ? p->kc.dw_r_wps : 1);
       s = cuda_err(cudaLaunchKernel((const void*)p->k_unfold, dim3(p->t.E, (p->t.K + 31) / 32), dim3(512), args,
                                     p->unfold_smem, st), "launch symcon_unfold");
       if (s) return s;

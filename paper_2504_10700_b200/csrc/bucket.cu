@@ -444,12 +444,12 @@ int fill_nan_launch(const int* perm, const int* seg_off, int E, float* out, long
 // element are contiguous). One thread per (z, j, k); 4-way unrolled loads for memory parallelism,
 // summed in item order so the result is bitwise deterministic.
 __global__ void dw_reduce_items(const float* __restrict__ spart, const int* __restrict__ item_off, int npad, int K,
-                                float* __restrict__ stot) {
+                                float* __restrict__ stot, int ppi) {
   const int z = blockIdx.y;
   const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long per = (long long)npad * K;
   if (slot >= per) return;
-  const int it0 = item_off[z], it1 = item_off[z + 1];
+  const int it0 = item_off[z] * ppi, it1 = item_off[z + 1] * ppi;   // ppi partials per item, in order
   // 8 independent partial sums (loads in flight together), combined in a fixed order
   float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   int it = it0;
@@ -462,10 +462,11 @@ __global__ void dw_reduce_items(const float* __restrict__ spart, const int* __re
   stot[(long long)z * per + slot] = s;
 }
 
-int reduce_items_launch(const float* spart, const int* item_off, int E, int npad, int K, float* stot, cudaStream_t st) {
+int reduce_items_launch(const float* spart, const int* item_off, int E, int npad, int K, float* stot, cudaStream_t st,
+                        int parts_per_item) {
   const long long per = (long long)npad * K;
   dim3 grid((unsigned)((per + 255) / 256), E);
-  dw_reduce_items<<<grid, 256, 0, st>>>(spart, item_off, npad, K, stot);
+  dw_reduce_items<<<grid, 256, 0, st>>>(spart, item_off, npad, K, stot, parts_per_item);
   return 1;
 }
 

@@ -31,7 +31,8 @@ int bucket_launch(const BucketArgs& a, cudaStream_t st);   // returns launches i
 int fill_nan_launch(const int* perm, const int* seg_off, int E, float* out, long long row, cudaStream_t st);
 size_t bucket_chunks(int64_t N);
 // stot[z][j][k] = sum over items it of element z (item order) of spart[it][j][k]
-int reduce_items_launch(const float* spart, const int* item_off, int E, int npad, int K, float* stot, cudaStream_t st);
+int reduce_items_launch(const float* spart, const int* item_off, int E, int npad, int K, float* stot, cudaStream_t st,
+                        int parts_per_item = 1);
 
 // dW all-reduce over peer memory (peer.cu)
 struct PeerArgs {
