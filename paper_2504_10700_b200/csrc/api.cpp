@@ -38,6 +38,7 @@ struct symcon_plan {
   int dw_gpc = 1, dw_nz = 1, dw2_gpc = 1, dw2_nz = 1;
   int grid_fwd = 0, grid_dA = 0, grid_bwd2 = 0, grid_fwd_r = 0;
   int rnq = 0;                 // fwd_r: coefficient quads per output slot
+  int warp_slots_dA_g = 0;     // gamma dA: resident warps over the GPU (tile split heuristic)
   size_t fwd_r_smem = 0;
   size_t simple_smem = 0;                               // simple plans: dynamic smem of fwd / dA
   std::string source;
@@ -412,16 +413,18 @@ static symcon_status build_common(int lmax_in, int corr, const int* out_L, int n
     for (auto& h : horner_vslots(p->t, p->kc.fwd_r_split)) p->rnq = std::max(p->rnq, (int)((h.rows.size() + 3) / 4));
     if (p->t.n_lm != 16) p->kc.fwd_r = 0;   // the A staging is laid out for 16 floats per (node, channel) (lmax_in 3)
   }
-  // measured (profiles/r02): dW_r -22% at MP-medium (4 slots); slower with 1 slot (OFF) and 9 (large)
-  if (p->kc.dw_r < 0) p->kc.dw_r = (p->t.out_per_ch >= 2 && p->t.out_per_ch <= 4) ? 1 : 0;
+  // measured (profiles/r02): dW_r -22% at MP-medium (4 slots), OFF-small (1 slot) step 0.154 vs 0.196 ms;
+  // slower at 9 slots (large)
+  if (p->kc.dw_r < 0) p->kc.dw_r = p->t.out_per_ch <= 4 ? 1 : 0;
   // dw_r stages 16-byte chunks of A rows (16 floats at lmax_in 3) and of 32-channel dB slices
   // (K % 32 != 0 falls back to symcon_bwd_dW at load time; the source does not depend on K)
   if (p->t.n_lm != 16) p->kc.dw_r = 0;
   if (p->kc.da_s < 0) p->kc.da_s = 0;
   if (p->kc.dw_r_block < 2 || 64 % p->kc.dw_r_block) { set_error("bad dw_r_block"); delete p; return SYMCON_EINVAL; }
-  // dW_r warps per slot: auto 4 with one output slot (a 1-warp CTA leaves too few warps per SM), else 1;
+  // dW_r warps per slot: measured at OFF-small (1 slot) the dW kernel alone is faster with 2 (0.042 vs
+  // 0.051 ms) but the step slower (0.186 vs 0.154 ms: less room for the concurrent dA) -> auto 1;
   // at most 16 warps per CTA
-  if (p->kc.dw_r_wps <= 0) p->kc.dw_r_wps = p->t.out_per_ch == 1 ? 4 : 1;
+  if (p->kc.dw_r_wps <= 0) p->kc.dw_r_wps = 1;
   if (32 * p->t.out_per_ch * std::max(1, p->kc.dw_r_split) * p->kc.dw_r_wps > 512) p->kc.dw_r_wps = 1;
   if (p->kc.dw_r_wps > p->kc.dw_r_block) { set_error("bad dw_r_wps"); delete p; return SYMCON_EINVAL; }
   if (p->kc.dw_r_wps > 1) { p->kc.unfold_reduce = 0; p->kc.dw_r_fuse = 0; }
@@ -517,6 +520,12 @@ symcon_status symcon_build_tables_ex(int lmax_in, int correlation, const int* ou
     if (!s) s = cuda_err(cudaLibraryGetKernel(&p->k_bwd2_dW, p->lib, "symcon_bwd2_dW"), "get symcon_bwd2_dW");
     if (!s && (p->kc.gamma & 1)) s = cuda_err(cudaLibraryGetKernel(&p->k_fwd_g, p->lib, "symcon_fwd_g"), "get symcon_fwd_g");
     if (!s && (p->kc.gamma & 2)) s = cuda_err(cudaLibraryGetKernel(&p->k_dA_g, p->lib, "symcon_bwd_dA_g"), "get symcon_bwd_dA_g");
+    if (!s && p->k_dA_g) {
+      int occ = 0, sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+      s = cuda_err(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)p->k_dA_g, 128, 0), "occupancy dA_g");
+      p->warp_slots_dA_g = sms * std::max(occ, 1) * 4;
+    }
     if (!s && p->kc.fwd_r) {
       s = cuda_err(cudaLibraryGetKernel(&p->k_fwd_r, p->lib, "symcon_fwd_r"), "get symcon_fwd_r");
       p->fwd_r_smem = sizeof(float) * p->kc.fwd_r_nst * (size_t)p->kc.fwd_r_block * 512 + 16 * p->kc.fwd_r_nst +
@@ -842,9 +851,14 @@ static symcon_status launch_dA_kernel(const symcon_plan* p, const WsLayout& w, P
   if (p->k_dA_s)
     return cuda_err(cudaLaunchKernel((const void*)p->k_dA_s, dim3(p->grid_dA_s), dim3(32 * p->kc.da_s_warps), args, p->da_s_smem, st),
                     "launch symcon_bwd_dA_s");
-  if (p->k_dA_g)
-    return cuda_err(cudaLaunchKernel((const void*)p->k_dA_g, dim3((unsigned)((w.max_tiles + 3) / 4), (p->t.K + 31) / 32), dim3(128),
+  if (p->k_dA_g) {
+    // warps split each tile's nodes (grid.z) when the tiles alone leave most warp slots empty
+    const long long warps = (long long)w.max_tiles * ((p->t.K + 31) / 32);
+    int split = p->kc.gamma_split;
+    if (split <= 0) split = (int)std::max<long long>(1, std::min<long long>(4, (p->warp_slots_dA_g + warps / 2) / std::max<long long>(warps, 1)));
+    return cuda_err(cudaLaunchKernel((const void*)p->k_dA_g, dim3((unsigned)((w.max_tiles + 3) / 4), (p->t.K + 31) / 32, split), dim3(128),
                                      args, 0, st), "launch symcon_bwd_dA_g");
+  }
   return cuda_err(cudaLaunchKernel((const void*)p->k_dA, dim3(p->grid_dA), dim3(32 * p->kc.tile_warps), args, p->tile_smem, st),
                   "launch symcon_bwd_dA");
 }

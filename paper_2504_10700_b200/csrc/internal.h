@@ -104,6 +104,7 @@ struct KernelConfig {
   int simple_warps = 4;      // simple plans (fp64 / corr 4): warps per fwd / dA CTA (coefficient rows in dynamic smem)
   int simple_unfold_split = 1;  // simple plans: column split of the unfold grid (grid.z)
   int fwd_r_split = 1;       // fwd_r: 2 = two warps per output slot (each half of the first indices), partial B summed in smem
+  int gamma_split = 0;       // gamma dA: warps per tile (grid.z) splitting its nodes; 0 auto (fill the GPU's warp slots)
   int dw_r_wps = 0;          // dW_r: warps per output slot (each its own partial over every wps-th node of a stage); 0 auto
   int fwd_r_wps = 0;         // fwd_r: warps per output slot, each taking every wps-th node pair of a stage; 0 auto
   int fwd_r_chains = 2;      // fwd_r: 2 (measured -2% fwd time) splits the Horner T / B accumulation chains into even / odd halves
