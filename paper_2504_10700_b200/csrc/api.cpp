@@ -855,7 +855,9 @@ static symcon_status launch_dA_kernel(const symcon_plan* p, const WsLayout& w, P
     // warps split each tile's nodes (grid.z) when the tiles alone leave most warp slots empty
     const long long warps = (long long)w.max_tiles * ((p->t.K + 31) / 32);
     int split = p->kc.gamma_split;
-    if (split <= 0) split = (int)std::max<long long>(1, std::min<long long>(4, (p->warp_slots_dA_g + warps / 2) / std::max<long long>(warps, 1)));
+    // measured at OFF-small: the step does not change with the split (dA runs concurrently with dW_r) -> auto 1
+    if (split <= 0) split = 1;
+    (void)warps;
     return cuda_err(cudaLaunchKernel((const void*)p->k_dA_g, dim3((unsigned)((w.max_tiles + 3) / 4), (p->t.K + 31) / 32, split), dim3(128),
                                      args, 0, st), "launch symcon_bwd_dA_g");
   }
