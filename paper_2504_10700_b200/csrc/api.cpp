@@ -174,6 +174,11 @@ size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 size_t esz(const symcon_plan* p) { return p->t.f64 ? sizeof(double) : sizeof(float); }
 
+// threads of a symcon_fwd_r CTA: (slots x split halves) / slot groups x warps per entry
+int fwd_r_threads(const symcon_plan* p) {
+  return 32 * p->t.out_per_ch * p->kc.fwd_r_split / std::max(1, p->kc.fwd_r_groups) * std::max(1, p->kc.fwd_r_wps);
+}
+
 // tiles per dW item for a call with N nodes: the plan's value, lowered for small N when the dW_r kernel
 // (one CTA per (item, 32-channel block), items processed serially) would otherwise be bound by its
 // longest item: at most N / (64 x the CTA slots per channel block) nodes per item (148 SMs x 3 CTAs)
@@ -409,6 +414,9 @@ static symcon_status build_common(int lmax_in, int corr, const int* out_L, int n
     // 4 warps sharing each stage's node pairs cut the forward 0.051 -> 0.036 ms
     if (p->kc.fwd_r_wps <= 0) p->kc.fwd_r_wps = p->t.out_per_ch == 1 ? 4 : 1;
     if (p->kc.fwd_r_split > 1) p->kc.fwd_r_wps = 1;
+    // slot groups (several CTAs per node block): auto 3 at 9 slots (large) -> 3 warps per CTA
+    if (p->kc.fwd_r_groups <= 0) p->kc.fwd_r_groups = (p->t.out_per_ch > 4 && p->t.out_per_ch % 3 == 0) ? 3 : 1;
+    if (p->kc.fwd_r_split > 1 || (p->t.out_per_ch * p->kc.fwd_r_split) % p->kc.fwd_r_groups) p->kc.fwd_r_groups = 1;
     if (p->kc.fwd_r_wps < 1 || p->kc.fwd_r_wps * p->kc.fwd_r_npw > p->kc.fwd_r_block / 2) { set_error("bad fwd_r_wps"); delete p; return SYMCON_EINVAL; }
     for (auto& h : horner_vslots(p->t, p->kc.fwd_r_split)) p->rnq = std::max(p->rnq, (int)((h.rows.size() + 3) / 4));
     if (p->t.n_lm != 16) p->kc.fwd_r = 0;   // the A staging is laid out for 16 floats per (node, channel) (lmax_in 3)
@@ -536,11 +544,11 @@ symcon_status symcon_build_tables_ex(int lmax_in, int correlation, const int* ou
                                                            (int)p->fwd_r_smem, device), "fwd_r smem attribute");
       int sms = 0, occ = 0;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-      if (!s) s = cuda_err(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)p->k_fwd_r,
-                                                                         32 * p->t.out_per_ch * p->kc.fwd_r_split * p->kc.fwd_r_wps,
+      if (!s) s = cuda_err(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)p->k_fwd_r, fwd_r_threads(p),
                                                                          p->fwd_r_smem), "occupancy fwd_r");
       if (p->kc.fwd_r_ctas_per_sm > 0) occ = std::min(occ, p->kc.fwd_r_ctas_per_sm);
       p->grid_fwd_r = sms * std::max(occ, 1);
+      p->grid_fwd_r -= p->grid_fwd_r % std::max(1, p->kc.fwd_r_groups);   // whole slot groups
     }
     if (!s && p->kc.da_s) {
       s = cuda_err(cudaLibraryGetKernel(&p->k_dA_s, p->lib, "symcon_bwd_dA_s"), "get symcon_bwd_dA_s");
@@ -831,8 +839,7 @@ static symcon_status launch_fwd_kernel(const symcon_plan* p, const WsLayout& w, 
   void* args[] = {&q};
   Timed tm(p, K_FWD, st);
   if (p->k_fwd_r)
-    return cuda_err(cudaLaunchKernel((const void*)p->k_fwd_r, dim3(p->grid_fwd_r),
-                                     dim3(32 * p->t.out_per_ch * p->kc.fwd_r_split * p->kc.fwd_r_wps), args, p->fwd_r_smem, st),
+    return cuda_err(cudaLaunchKernel((const void*)p->k_fwd_r, dim3(p->grid_fwd_r), dim3(fwd_r_threads(p)), args, p->fwd_r_smem, st),
                     "launch symcon_fwd_r");
   if (p->k_fwd_g)
     return cuda_err(cudaLaunchKernel((const void*)p->k_fwd_g, dim3((unsigned)((w.max_tiles + 3) / 4), (p->t.K + 31) / 32), dim3(128),
