@@ -433,7 +433,10 @@ static symcon_status build_common(int lmax_in, int corr, const int* out_L, int n
   // 0.051 ms) but the step slower (0.186 vs 0.154 ms: less room for the concurrent dA) -> auto 1;
   // at most 16 warps per CTA
   if (p->kc.dw_r_wps <= 0) p->kc.dw_r_wps = 1;
-  if (32 * p->t.out_per_ch * std::max(1, p->kc.dw_r_split) * p->kc.dw_r_wps > 512) p->kc.dw_r_wps = 1;
+  // dW_r row-group sets (grid.z): auto 3 at 9 slots (large), so a CTA holds 3 slot warps
+  if (p->kc.dw_r_groups <= 0) p->kc.dw_r_groups = (p->t.out_per_ch > 4 && p->t.out_per_ch % 3 == 0) ? 3 : 1;
+  if (p->kc.dw_r_fuse || (p->t.out_per_ch * std::max(1, p->kc.dw_r_split)) % p->kc.dw_r_groups) p->kc.dw_r_groups = 1;
+  if (32 * p->t.out_per_ch * std::max(1, p->kc.dw_r_split) * p->kc.dw_r_wps > 512 * std::max(1, p->kc.dw_r_groups)) p->kc.dw_r_wps = 1;
   if (p->kc.dw_r_wps > p->kc.dw_r_block) { set_error("bad dw_r_wps"); delete p; return SYMCON_EINVAL; }
   if (p->kc.dw_r_wps > 1) { p->kc.unfold_reduce = 0; p->kc.dw_r_fuse = 0; }
   if (p->t.simple) {   // fp64 or correlation 4: the plain scalar kernels of codegen_simple.cpp
@@ -986,8 +989,10 @@ static symcon_status backward_impl(const symcon_plan* p, int64_t N, const float*
     {
     Timed tm(p, K_DW, st);
     if (p->k_dW_r)   // S partials (+ with dw_r_fuse the element's item reduction and the unfold)
-      s = cuda_err(cudaLaunchKernel((const void*)p->k_dW_r, dim3((unsigned)(w.max_items + (p->kc.dw_r_fuse ? p->t.E : 0)), p->t.K / 32, 1),
-                                    dim3(32 * p->t.out_per_ch * std::max(1, p->kc.dw_r_split) * p->kc.dw_r_wps), args, p->dw_r_smem, st),
+      s = cuda_err(cudaLaunchKernel((const void*)p->k_dW_r,
+                                    dim3((unsigned)(w.max_items + (p->kc.dw_r_fuse ? p->t.E : 0)), p->t.K / 32, p->kc.dw_r_groups),
+                                    dim3(32 * p->t.out_per_ch * std::max(1, p->kc.dw_r_split) / p->kc.dw_r_groups * p->kc.dw_r_wps), args,
+                                    p->dw_r_smem, st),
                    "launch symcon_bwd_dW_r");
     else
       s = cuda_err(cudaLaunchKernel((const void*)p->k_dW, dim3((unsigned)(w.max_items * p->dw_nz), (p->t.K + 31) / 32, 1),

@@ -106,6 +106,7 @@ struct KernelConfig {
   int fwd_r_split = 1;       // fwd_r: 2 = two warps per output slot (each half of the first indices), partial B summed in smem
   int gamma_split = 0;       // gamma dA: warps per tile (grid.z) splitting its nodes; 0 auto (fill the GPU's warp slots)
   int dw_r_wps = 0;          // dW_r: warps per output slot (each its own partial over every wps-th node of a stage); 0 auto
+  int dw_r_groups = 0;       // dW_r: CTAs (grid.z) per (item, channel block), each a subset of the row groups; 0 auto
   int fwd_r_groups = 0;      // fwd_r: CTAs per node block, each serving 1/groups of the output slots; 0 auto
   int fwd_r_wps = 0;         // fwd_r: warps per output slot, each taking every wps-th node pair of a stage; 0 auto
   int fwd_r_chains = 2;      // fwd_r: 2 (measured -2% fwd time) splits the Horner T / B accumulation chains into even / odd halves
