@@ -421,9 +421,9 @@ static symcon_status build_common(int lmax_in, int corr, const int* out_L, int n
     for (auto& h : horner_vslots(p->t, p->kc.fwd_r_split)) p->rnq = std::max(p->rnq, (int)((h.rows.size() + 3) / 4));
     if (p->t.n_lm != 16) p->kc.fwd_r = 0;   // the A staging is laid out for 16 floats per (node, channel) (lmax_in 3)
   }
-  // measured (profiles/r02): dW_r -22% at MP-medium (4 slots), OFF-small (1 slot) step 0.154 vs 0.196 ms;
-  // slower at 9 slots (large)
-  if (p->kc.dw_r < 0) p->kc.dw_r = p->t.out_per_ch <= 4 ? 1 : 0;
+  // measured (profiles/r02): dW_r -22% at MP-medium (4 slots), OFF-small (1 slot) step 0.154 vs 0.196 ms,
+  // large (9 slots, as 3 row-group sets) dW 4.84 vs 5.97 ms (with dA after dW, dist.DataParallelContraction)
+  if (p->kc.dw_r < 0) p->kc.dw_r = 1;
   // dw_r stages 16-byte chunks of A rows (16 floats at lmax_in 3) and of 32-channel dB slices
   // (K % 32 != 0 falls back to symcon_bwd_dW at load time; the source does not depend on K)
   if (p->t.n_lm != 16) p->kc.dw_r = 0;

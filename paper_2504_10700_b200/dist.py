@@ -103,9 +103,11 @@ class DataParallelContraction:
         self._peer = None
         self._peer2 = None
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
-        # measured (profiles/r01): dA concurrent with dW helps at N=1 (+2-4%) and is the default at
-        # every N (the dW all-reduce then runs as SMs free up)
-        self.concurrent_bwd = True if concurrent_bwd is None else concurrent_bwd
+        # measured: dA concurrent with dW helps with <= 4 output slots per channel (MP-medium 1.08 vs
+        # 1.12 ms/step; the dW all-reduce then runs as SMs free up); at 9 slots (large) the 3-CTA-per-item
+        # dW_r and the persistent dA slow each other down (21.6 vs 18.2 ms), so dA follows dW there
+        out_slots = sc.out_dim // max(sc.channels, 1)
+        self.concurrent_bwd = (out_slots <= 4) if concurrent_bwd is None else concurrent_bwd
         self.side = torch.cuda.Stream(device=sc.device) if self.concurrent_bwd else None
         self.comm = torch.cuda.Stream(device=sc.device) if self.world > 1 else None
         self.launches = 0
