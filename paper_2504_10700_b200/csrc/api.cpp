@@ -1002,7 +1002,8 @@ static symcon_status backward_impl(const symcon_plan* p, int64_t N, const float*
     if (!p->k_dW_r || !p->kc.dw_r_fuse) {
       Timed tm(p, K_UNFOLD, st);
       if (!p->kc.unfold_reduce)
-        n += reduce_items_launch(q.spart, q.item_off, p->t.E, p->npad, p->t.K, q.stot, st, p->k_dW_r ? p->kc.dw_r_wps : 1);
+        n += reduce_items_launch(q.spart, q.item_off, p->t.E, p->npad, p->t.K, q.stot, st,
+                                 !p->k_dW_r ? 1 : (p->kc.dw_r_wps == 1 && !p->kc.dw_r_fuse) ? -1 : p->kc.dw_r_wps);
       s = cuda_err(cudaLaunchKernel((const void*)p->k_unfold, dim3(p->t.E, (p->t.K + 31) / 32), dim3(512), args,
                                     p->unfold_smem, st), "launch symcon_unfold");
       if (s) return s;

@@ -445,11 +445,15 @@ int fill_nan_launch(const int* perm, const int* seg_off, int E, float* out, long
 // summed in item order so the result is bitwise deterministic.
 __global__ void dw_reduce_items(const float* __restrict__ spart, const int* __restrict__ item_off, int npad, int K,
                                 float* __restrict__ stot, int ppi) {
+  // ppi < 0: single-item elements were written straight into stot by the dW kernel (skip them)
+  const bool skip_single = ppi < 0;
+  if (skip_single) ppi = 1;
   const int z = blockIdx.y;
   const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long per = (long long)npad * K;
   if (slot >= per) return;
   const int it0 = item_off[z] * ppi, it1 = item_off[z + 1] * ppi;   // ppi partials per item, in order
+  if (skip_single && it1 - it0 == 1) return;
   // 8 independent partial sums (loads in flight together), combined in a fixed order
   float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   int it = it0;

@@ -32,7 +32,7 @@ int fill_nan_launch(const int* perm, const int* seg_off, int E, float* out, long
 size_t bucket_chunks(int64_t N);
 // stot[z][j][k] = sum over items it of element z (item order) of spart[it][j][k]
 int reduce_items_launch(const float* spart, const int* item_off, int E, int npad, int K, float* stot, cudaStream_t st,
-                        int parts_per_item = 1);
+                        int parts_per_item = 1);   // parts_per_item -1: one part per item, single-item elements already in stot
 
 // dW all-reduce over peer memory (peer.cu)
 struct PeerArgs {
