@@ -570,7 +570,8 @@ symcon_status symcon_build_tables_ex(int lmax_in, int correlation, const int* ou
       for (int L : p->t.out_L) dbw += 32 * (2 * L + 1);
       p->dw_r_smem = sizeof(float) * p->kc.dw_r_nst * (size_t)p->kc.dw_r_block * (512 + dbw) + 16 * p->kc.dw_r_nst +
                      sizeof(int) * (p->kc.dw_r_nst * (size_t)p->kc.dw_r_block + 1);
-      if (p->kc.dw_r_fuse) p->dw_r_smem = std::max(p->dw_r_smem, sizeof(float) * (size_t)p->npad * 33);   // the S table aliases the ring
+      if (p->kc.dw_r_fuse || p->kc.dw_r_unfold_single)
+        p->dw_r_smem = std::max(p->dw_r_smem, sizeof(float) * (size_t)p->npad * 33);   // the S table aliases the ring
       if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_dW_r, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                            (int)p->dw_r_smem, device), "dW_r smem attribute");
     }
@@ -966,6 +967,9 @@ static symcon_status backward_impl(const symcon_plan* p, int64_t N, const float*
   int n = launch_prep(p, w, (char*)ws, N, ne, W, q, st, dA != nullptr, &s, flags);
   if (s) return s;
   if (dW && p->k_dW_r && (s = encode_a_map(q.tmA, A, N, p->t.K, p->t.n_lm))) return s;
+  // single-item elements finished (unfolded) by their dW_r CTA: the unfold kernel skips them
+  q.pad = (dW && p->k_dW_r && p->kc.dw_r_unfold_single && p->kc.dw_r_wps == 1 && p->kc.dw_r_groups == 1 && !p->kc.dw_r_fuse &&
+           !p->kc.unfold_reduce) ? 1 : 0;
   void* args[] = {&q};
   const unsigned ky = (p->t.K + p->kc.warps_per_cta - 1) / p->kc.warps_per_cta;
   if (dW && p->t.simple) {   // simple plans: S partials (item, row group, channel block), item reduction, unfold
