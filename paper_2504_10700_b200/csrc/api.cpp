@@ -445,6 +445,10 @@ static symcon_status build_common(int lmax_in, int corr, const int* out_L, int n
     // table-driven fold / unfold: split rows / columns over grid.z (~256 per CTA)
     p->kc.fold_split = std::min(16, std::max(1, p->npad / 256));
     p->kc.simple_unfold_split = std::min(16, std::max(1, (int)p->t.paths.size() / 64));
+    // dW rows per warp: fewer row groups = fewer re-reads of each node's A row; measured (profiles/r02):
+    // fp64 MP-medium dW 1.63 ms at 96 vs 2.68 ms at 48 (128 spills); correlation 4 fp32 2.84 ms at 128
+    // vs 5.97 ms at 48 (192: same as 128)
+    if (p->kc.simple_rpg <= 0) p->kc.simple_rpg = p->t.f64 ? 96 : 128;
     // coefficient rows of the SWPC warps of a fwd / dA CTA in dynamic shared memory (<= 200 KB)
     const size_t row_bytes = esz(p) * (size_t)p->npad;
     p->kc.simple_warps = 4;
@@ -975,7 +979,7 @@ static symcon_status backward_impl(const symcon_plan* p, int64_t N, const float*
   if (dW && p->t.simple) {   // simple plans: S partials (item, row group, channel block), item reduction, unfold
     {
       Timed tm(p, K_DW, st);
-      const int ng = ((int)p->t.rows.size() + 47) / 48;   // = codegen_simple RPG 48
+      const int rpg = std::max(8, p->kc.simple_rpg), ng = ((int)p->t.rows.size() + rpg - 1) / rpg;   // = codegen_simple RPG
       s = cuda_err(cudaLaunchKernel((const void*)p->k_dW, dim3((unsigned)w.max_items, ng, (p->t.K + 31) / 32), dim3(32), args, 0, st),
                    "launch symcon_bwd_dW (simple)");
     }
