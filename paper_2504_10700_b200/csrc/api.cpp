@@ -574,8 +574,12 @@ symcon_status symcon_build_tables_ex(int lmax_in, int correlation, const int* ou
       for (int L : p->t.out_L) dbw += 32 * (2 * L + 1);
       p->dw_r_smem = sizeof(float) * p->kc.dw_r_nst * (size_t)p->kc.dw_r_block * (512 + dbw) + 16 * p->kc.dw_r_nst +
                      sizeof(int) * (p->kc.dw_r_nst * (size_t)p->kc.dw_r_block + 1);
-      if (p->kc.dw_r_fuse || p->kc.dw_r_unfold_single)
-        p->dw_r_smem = std::max(p->dw_r_smem, sizeof(float) * (size_t)p->npad * 33);   // the S table aliases the ring
+      // the S table of the fused reduction / the single-item unfold aliases the ring (same condition as the
+      // codegen's: with row-group sets a CTA never unfolds, and must not pay the larger smem)
+      const bool unf1 = p->kc.dw_r_unfold_single && p->kc.dw_r_wps == 1 && p->kc.dw_r_groups == 1 && !p->kc.dw_r_fuse &&
+                        !p->kc.unfold_reduce;
+      if (p->kc.dw_r_fuse || unf1)
+        p->dw_r_smem = std::max(p->dw_r_smem, sizeof(float) * (size_t)p->npad * 33);
       if (!s) s = cuda_err(cudaKernelSetAttributeForDevice(p->k_dW_r, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                            (int)p->dw_r_smem, device), "dW_r smem attribute");
     }
