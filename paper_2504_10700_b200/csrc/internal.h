@@ -105,6 +105,7 @@ struct KernelConfig {
   int simple_unfold_split = 1;  // simple plans: column split of the unfold grid (grid.z)
   int simple_rpg = 0;        // simple plans: dW rows per warp (register accumulators); 0 auto (fp32 128, fp64 96)
   int fwd_r_split = 1;       // fwd_r: 2 = two warps per output slot (each half of the first indices), partial B summed in smem
+  int fwd_r_prod_light = 1;  // fwd_r: the TMA producer is the warp of the lightest slot (else the CTA's warp 0)
   int dw_r_prod_light = 1;   // dW_r: the TMA producer is the warp with the lightest row group (else row group 0)
   int dw_r_unfold_single = 1;   // dW_r CTAs of single-item elements unfold dW themselves (skipped by reduce / unfold)
   int gamma_split = 0;       // gamma dA: warps per tile (grid.z) splitting its nodes; 0 auto (fill the GPU's warp slots)
