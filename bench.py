@@ -85,6 +85,13 @@ def parse(argv=None):
 
 
 # ----------------------------------------------------------------------------- workload
+def needs_l2_flush(step_input_bytes, pool_bytes, l2_bytes=L2_BYTES):
+    """Timing rule: between timed steps either flush L2 or use inputs larger than L2. No flush when a
+    step's own inputs exceed L2 or the pool of distinct bins cycled through is > 3x L2 (each step's
+    inputs were evicted by the other bins' traffic); otherwise flush before every step."""
+    return not (step_input_bytes > l2_bytes or pool_bytes > 3 * l2_bytes)
+
+
 def shape_of(name, correlation=None):
     import dataclasses
     from synth.inputs import CONFIGS
@@ -621,7 +628,7 @@ def run_ours(args):
     # outside that step's own event pair, and the step times are summed
     step_in = max(x[2].nbytes + x[3].nbytes + x[4].nbytes for x in pool)
     pool_bytes = sum(x[2].nbytes + x[3].nbytes + x[4].nbytes + x[5].nbytes + x[6].nbytes for x in pool)
-    flush = not (step_in > L2_BYTES or pool_bytes > 3 * L2_BYTES)
+    flush = needs_l2_flush(step_in, pool_bytes)
     scratch = torch.empty(int(2 * L2_BYTES), dtype=torch.uint8, device=dev) if flush else None
     # per-step event pairs (median / min per step beside the mean the line's value uses)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]

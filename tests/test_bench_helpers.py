@@ -63,3 +63,15 @@ def test_alg_ops_trie_generalises_alg_ops(L):
         else:
             assert t["fwd"] == t["trie_nodes"] and t["path"] == t["fwd"] + t["dA"] + t["dW"]
         L.symcon_destroy(s.plan)
+
+
+def test_l2_flush_policy():
+    """bench.py's L2 rule (the contract: flush L2 between timed steps or use inputs larger than L2):
+    MP-medium 50k bins (512 MB of inputs per step) and OFF-small (131 MB > 126 MB) need no flush; the
+    C = 3,072 pool (31 MB per step, 252 MB over 4 bins) is flushed."""
+    import bench
+    MB = 1e6
+    assert not bench.needs_l2_flush(512 * MB, 4 * 1100 * MB)     # MP-medium, C = 50,000
+    assert not bench.needs_l2_flush(131 * MB, 4 * 262 * MB)      # OFF-small molecule batches
+    assert bench.needs_l2_flush(31 * MB, 252 * MB)               # C = 3,072
+    assert not bench.needs_l2_flush(31 * MB, 400 * MB)           # a pool > 3x L2 evicts itself
