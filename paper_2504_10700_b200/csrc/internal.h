@@ -106,6 +106,7 @@ struct KernelConfig {
   int simple_rpg = 0;        // simple plans: dW rows per warp (register accumulators); 0 auto (fp32 128, fp64 96)
   int fwd_r_split = 1;       // fwd_r: 2 = two warps per output slot (each half of the first indices), partial B summed in smem
   int fwd_r_prod_light = 1;  // fwd_r: the TMA producer is the warp of the lightest slot (else the CTA's warp 0)
+  int dw_r_balance = 0;      // dW_r: warps take (slot, first index) units balanced by op count instead of whole slots
   int dw_r_prod_light = 1;   // dW_r: the TMA producer is the warp with the lightest row group (else row group 0)
   int dw_r_unfold_single = 1;   // dW_r CTAs of single-item elements unfold dW themselves (skipped by reduce / unfold)
   int gamma_split = 0;       // gamma dA: warps per tile (grid.z) splitting its nodes; 0 auto (fill the GPU's warp slots)
@@ -123,7 +124,7 @@ std::string generate_source_simple(const Tables& t, const KernelConfig& kc);
 
 // Horner program of one output slot (symcon_fwd_r)
 struct HornerB { int b, row_ab; std::vector<std::pair<int, int>> cs; };   // (c, row j) of degree-3 rows
-struct HornerA { int a, row_a; std::vector<HornerB> bs; };
+struct HornerA { int a, row_a; std::vector<HornerB> bs; int slot = -1; };   // slot: set when a warp mixes slots
 struct HornerSlot { int slot; std::vector<HornerA> as; std::vector<int> rows; int half = 0; };  // rows: register order
 std::vector<HornerSlot> horner_slots(const Tables& t);
 // fwd_r warps: the slots, or (fwd_r_split = 2) each slot's first indices split in two op-balanced halves
