@@ -310,6 +310,10 @@ symcon_status symcon_tp_backward(const symcon_tp_plan* plan, int64_t num_nodes, 
  * receiver pointers, N and E; the caller guarantees the index arrays are unchanged since that call
  * (e.g. the backward of a step after its forward). Otherwise (or on any mismatch) it is rebuilt. */
 #define SYMCON_TP_REUSE_GRAPH 4u
+/* Forward flag: also build the backward's sender CSR into `ws`, on an internal stream concurrently with
+ * the forward kernel (joined before the call's work on `stream` completes); a following backward with
+ * SYMCON_TP_REUSE_GRAPH then builds nothing. */
+#define SYMCON_TP_PREP_BACKWARD 8u
 symcon_status symcon_tp_forward_ex(const symcon_tp_plan* plan, int64_t num_nodes, int64_t num_edges,
                                    const float* Y, const float* h, const float* R, const int32_t* sender,
                                    const int32_t* receiver, float* A, void* ws, size_t ws_bytes, uint32_t flags,

@@ -329,6 +329,7 @@ def symcon_tp_backward2(plan, N, E, Y, h, R, sender, receiver, dA, uY, uh, uR, d
 
 
 SYMCON_TP_REUSE_GRAPH = 4
+SYMCON_TP_PREP_BACKWARD = 8
 lib.symcon_tp_forward_ex.argtypes = [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, ctypes.c_uint32, _vp]
 lib.symcon_tp_forward_ex.restype = ctypes.c_int
 lib.symcon_tp_backward_ex.argtypes = [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz,

@@ -226,14 +226,17 @@ class ChannelwiseTP:
         assert sender.dtype == torch.int32 and receiver.dtype == torch.int32 and receiver.shape == (E,)
         return N, E
 
-    def forward_raw(self, Y, h, R, sender, receiver, A=None):
+    def forward_raw(self, Y, h, R, sender, receiver, A=None, prep_backward=False):
+        """prep_backward=True: also build the backward's sender CSR (SYMCON_TP_PREP_BACKWARD), concurrently
+        with the forward kernel, for a following backward_raw(..., reuse=True)."""
         N, E = self._check(Y, h, R, sender, receiver)
         if A is None:
             A = torch.empty((N, self.channels, self.n_out), dtype=torch.float32, device=self.device)
         ws = self.workspace(N, E)
         ptr = lambda t: t.data_ptr() if t.numel() else None
         _lib.symcon_tp_forward(self.plan, N, E, ptr(Y), ptr(h), ptr(R), ptr(sender), ptr(receiver), A.data_ptr(),
-                               ws.data_ptr(), ws.numel(), _stream_ptr(self.device))
+                               ws.data_ptr(), ws.numel(), _stream_ptr(self.device),
+                               _lib.SYMCON_TP_PREP_BACKWARD if prep_backward else 0)
         return A
 
     def backward_raw(self, Y, h, R, sender, receiver, dA, need_Y=True, need_h=True, need_R=True, reuse=False):

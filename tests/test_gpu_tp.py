@@ -218,6 +218,16 @@ def test_tp_graph_reuse_flag():
     for a, b, c in zip(ref, got, got2):
         assert torch.equal(a, b) and torch.equal(a, c)
     assert n_reuse2 < n_reuse1 < n_full, (n_full, n_reuse1, n_reuse2)
+    # SYMCON_TP_PREP_BACKWARD: the forward builds the sender CSR concurrently; the backward builds nothing
+    A0 = tp.forward_raw(Y, h, R, s, r)
+    A1 = tp.forward_raw(Y, h, R, s, r, prep_backward=True)
+    got3 = tp.backward_raw(Y, h, R, s, r, dA, reuse=True)
+    n_prep = tp.last_launch_count()
+    torch.cuda.synchronize()
+    assert torch.equal(A0, A1)
+    for a, c in zip(ref, got3):
+        assert torch.equal(a, c)
+    assert n_prep == n_reuse2, (n_prep, n_reuse2)
     # another graph (new index tensors) with the flag: must not reuse the old structure
     from synth.inputs import gen_tp_graph
     sizes2 = [25, 47]
